@@ -1,0 +1,403 @@
+"""Benchmark: CONCORD-PCD on B200 vs the reference CPU path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the paper workload): AR(2) truth,
+p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
+the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = one complete
+cold-start CONCORD-PCD fit (identity init, delta_tol 1e-5) at the next lambda
+of the path; K=10 covers the whole path.  The metric is sweeps/s (outer
+iterations per second, BASELINE "sweeps/sec"), with seconds-to-converge per
+lambda reported beside it.
+
+* value: device time (CUDA events on the solver's stream) with T resident in
+  HBM; the W/T/Omega working set (3 x 200 MB) exceeds the 126 MB L2.
+* e2e: the same metric through the public API `pcd_fit(GramMatrix, SolverConfig)`
+  with T in pinned host memory: every step uploads T (H2D) and reads Omega back (D2H).
+* roofline: pcd_wform_kernel's algorithmic bytes per launch / its event time.
+* cpu_baseline / --impl reference: the reference's own compiled sweep
+  (oracle/_ref, built from /root/reference's _ckernels.pyx) on all host cores,
+  timed on a bounded sample of rounds (sweep cost is data-independent).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+LAMS = [0.55, 0.50, 0.45, 0.40, 0.35, 0.30, 0.25, 0.20, 0.15, 0.10]
+METRIC = "sweeps/s (CONCORD-PCD fits, p=5000 n=2000, 10-lambda path)"
+UNIT = "sweeps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--p", type=int, default=5000)
+    ap.add_argument("--n", type=int, default=2000)
+    ap.add_argument("--delta-tol", type=float, default=1e-5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- plumbing
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend="nccl"):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v):
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([float(v)], device=f"cuda:{self.local}", dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v):
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([float(v)], device=f"cuda:{self.local}", dtype=torch.float64)
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi samples of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get(workload)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def make_problem(p, n):
+    from paper_2106_09382_b200 import synth
+
+    return synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
+
+
+def algorithmic_bytes(p, nnz_per_sweep, want_trace=True):
+    """colour k moves 48*p*nnz_k + 24*p bytes, the diagonal step 24*p^2
+    (+8*p^2 for the fused objective's Omega read)."""
+    pe = p + (p % 2)
+    per_sweep_fixed = 24.0 * p * (pe - 1) + 24.0 * p * p + (8.0 * p * p if want_trace else 0.0)
+    return sum(48.0 * p * float(k) + per_sweep_fixed for k in nnz_per_sweep)
+
+
+# --------------------------------------------------------------- CPU reference
+
+
+def cpu_reference_rate(t, n, lam, target_s, workers):
+    """Sweeps/s of the reference's compiled pcd_sweep on a bounded sample of rounds."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as orc
+
+    ref = orc.load_ref()
+    kind = "reference" if ref is not None else "port"
+    p = t.shape[0]
+    rs, ss, off = orc.circle_flat(p)
+    nrounds = off.shape[0] - 1
+
+    def run(k0, k1):
+        om = np.eye(p)
+        sub = off[k0:k1 + 1]
+        tic = time.perf_counter()
+        if ref is not None:
+            ref.pcd_sweep(om, t, float(n), n * lam, rs.astype(np.intp), ss.astype(np.intp), sub.astype(np.intp),
+                          int(workers))
+        else:
+            orc.pcd_sweep(om, t, n, n * lam, rs, ss, sub, workers)
+        return time.perf_counter() - tic
+
+    probe = max(2, min(nrounds, 8))
+    dt = run(0, probe)
+    rounds = int(max(probe, min(nrounds, target_s / max(dt / probe, 1e-9))))
+    el = run(0, rounds)
+    # each call also runs the p diagonal updates (1/p of a sweep) -- counted as work done
+    return (rounds / nrounds) / el, kind, rounds, el
+
+
+# --------------------------------------------------------------- our arm
+
+
+def run_ours(args, d):
+    import torch
+
+    import paper_2106_09382_b200 as cb
+    from paper_2106_09382_b200 import _lib
+
+    torch.cuda.set_device(d.local)
+    p, n, K, W = args.p, args.n, args.steps, args.warmup
+    x = make_problem(p, n)
+    stream = torch.cuda.Stream()
+    s = cb.Solver(p, device=d.local)
+    s.set_stream(stream.cuda_stream)
+    g0 = time.perf_counter()
+    s.gram_from_data(cb.DataMatrix(x, centered=True))
+    gram_s = time.perf_counter() - g0
+
+    def lam_at(step):
+        return LAMS[(d.rank + step * d.world) % len(LAMS)]
+
+    def one_fit(lam):
+        rc, res, deltas, objs, secs = s.fit_raw(lam, args.delta_tol, 5000, trace=True)
+        nnz = np.zeros(res.iterations, dtype=np.int64)
+        cnt = ctypes_int()
+        _lib.check(_lib.load().concord_solver_sweep_stats(s._h, _lib.ptr(nnz), res.iterations, cnt))
+        return res, nnz
+
+    for i in range(W):
+        one_fit(lam_at(i))
+    clocks = Clocks(d.local)
+    d.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fits = []
+    for i in range(K):
+        lam = lam_at(i)
+        res, nnz = one_fit(lam)
+        fits.append((lam, int(res.iterations), float(res.kernel_ms), nnz, bool(res.converged), int(res.edge_count),
+                     int(res.n_blocks), int(res.slab_width)))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    d.barrier()
+    clk = clocks.stop()
+    elapsed_ms = d.max(e0.elapsed_time(e1))
+    sweeps = d.sum(sum(f[1] for f in fits))
+    value = sweeps / (elapsed_ms / 1e3)
+
+    # roofline of the dominant kernel (pcd_wform_kernel), per launch
+    kern_ms = [f[2] for f in fits]
+    bytes_per = [algorithmic_bytes(p, f[3]) for f in fits]
+    avg_ms = sum(kern_ms) / len(kern_ms)
+    avg_bytes = sum(bytes_per) / len(bytes_per)
+    peak, peak_src = measured_peak_hbm()
+    achieved = avg_bytes / (avg_ms / 1e3) / 1e9
+    workload = f"ar2 p={p} n={n} lambda-path cold"
+    traffic = ncu_traffic(workload)
+    nnz_frac = [float(f[3].sum()) / (f[1] * (p * (p - 1) / 2)) for f in fits]
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
+        "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: AR(2) truth (datagen.ar2_precision), X ~ N(0, inv(truth)) n=2000 seed 0, centred",
+        "config": {"workload": workload, "source": "BASELINE.json configs[2] (paper workload)", "p": p, "n": n,
+                   "lambdas": [lam_at(i) for i in range(K)], "delta_tol": args.delta_tol, "init": "identity",
+                   "l2": "inputs larger than L2 (T, W, Omega slabs 3 x %.0f MB > 126 MB)" % (8 * p * p / 1e6),
+                   "parallelism": f"{d.world} GPU(s), independent lambda fits per GPU" if d.world > 1 else
+                   "1 GPU, persistent cooperative kernel", "n_blocks": fits[0][6], "slab_width": fits[0][7]},
+        "seconds_to_converge": {f"{f[0]:.2f}": round(f[2] / 1e3, 6) for f in fits},
+        "iterations": {f"{f[0]:.2f}": f[1] for f in fits},
+        "edges": {f"{f[0]:.2f}": f[5] for f in fits},
+        "nonzero_pair_fraction": {f"{f[0]:.2f}": round(v, 6) for f, v in zip(fits, nnz_frac)},
+        "gram_s_incl_h2d": round(gram_s, 4),
+        "roofline": {"kernel": "pcd_wform_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
+                     "note": "bytes = sum over sweeps of 48p*nnz_k per colour + 24p per colour + 32p^2 diag/objective"},
+        "gpu_launches": 3 * K,
+        "clocks": clk,
+    }
+
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, d, s, stream, lam_at)
+    if not args.no_cpu and d.world == 1 and d.rank == 0:
+        t_host = s.gram().t
+        rate, kind, rounds, el = cpu_reference_rate(t_host, n, 0.3, args.cpu_seconds, os.cpu_count())
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                               "sample": f"{rounds} of {p + (p % 2) - 1} colour rounds of one pcd_sweep at p={p} "
+                                         f"(workers={os.cpu_count()}), {el:.1f} s; sweep cost is data-independent"}
+        iters_total = sum(f[1] for f in fits)
+        out["cpu_baseline"]["seconds_to_converge_extrapolated"] = iters_total / rate
+    s.close()
+    return out
+
+
+def ctypes_int():
+    import ctypes
+
+    return ctypes.byref(ctypes.c_int32(0))
+
+
+def run_e2e(args, d, s, stream, lam_at):
+    """Same metric through pcd_fit(GramMatrix host, SolverConfig): H2D T + fit + D2H Omega per step."""
+    import torch
+
+    import paper_2106_09382_b200 as cb
+    from paper_2106_09382_b200 import _lib
+
+    p, n, K, W = args.p, args.n, args.steps, args.warmup
+    t_pinned = _lib.pinned_empty((p, p))
+    t_pinned[...] = s.gram().t
+    gram = cb.GramMatrix(t_pinned, n)  # validated once, as a user would construct it
+    for i in range(min(W, 2)):
+        cb.pcd_fit(gram, cb.SolverConfig(lam=lam_at(i), max_outer_iterations=5000), device=d.local)
+    d.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sweeps = 0
+    for i in range(K):
+        rep = cb.pcd_fit(gram, cb.SolverConfig(lam=lam_at(i), max_outer_iterations=5000), device=d.local)
+        sweeps += rep.iterations
+    e1.record()
+    torch.cuda.synchronize()
+    d.barrier()
+    el = d.max(e0.elapsed_time(e1))
+    total = d.sum(sweeps)
+    return {"value": total / (el / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * p * p,
+            "d2h_bytes_per_step": 8 * p * p, "ms_per_step": el / K,
+            "path": "paper_2106_09382_b200.pcd_fit(GramMatrix(pinned T), SolverConfig(lam)) -> FitReport"}
+
+
+# --------------------------------------------------------------- reference arm
+
+
+def run_reference(args, d):
+    if d.rank != 0:
+        return None
+    from paper_2106_09382_b200 import synth
+
+    p, n, K, W = args.p, args.n, args.steps, args.warmup
+    t = synth.host_gram(make_problem(p, n))
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    per_step = max(1.0, min(args.cpu_seconds, 150.0 / max(K + W, 1)))
+    rates = []
+    kind = None
+    info = None
+    for i in range(W + K):
+        rate, kind, rounds, el = cpu_reference_rate(t, n, LAMS[i % len(LAMS)], per_step, os.cpu_count())
+        if i >= W:
+            rates.append((rate, rounds, el))
+        info = (rounds, el)
+    total_sweeps = sum(r[1] / (p + (p % 2) - 1) for r in rates)
+    total_s = sum(r[2] for r in rates)
+    value = total_sweeps / total_s
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "impl": "reference",
+            "data": "synthetic: AR(2) truth, X ~ N(0, inv(truth)) n=2000 seed 0, centred",
+            "config": {"workload": f"ar2 p={p} n={n} lambda-path cold", "p": p, "n": n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                             "sample": f"each step = {info[0]} colour rounds of the reference pcd_sweep "
+                                       f"(compiled _ckernels, workers={os.cpu_count()}); sweeps = rounds/{p - 1 + p % 2}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def main():
+    args = parse()
+    d = Dist()
+    if args.impl == "reference":
+        out = run_reference(args, d)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    d.init("nccl")
+    try:
+        out = run_ours(args, d)
+    finally:
+        d.close()
+    if d.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

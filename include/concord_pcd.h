@@ -1,0 +1,120 @@
+/*
+ * concord_pcd.h -- C ABI of the B200-native CONCORD-PCD solver
+ * (libconcord_b200.so, built from paper_2106_09382_b200/csrc/).
+ *
+ * Drop-in boundary for the reference package `parconcord`
+ * (/root/reference/pkg/src/parconcord).  Plain pointers and sizes only; no
+ * C++ exceptions or torch types cross this boundary.  Every function returns
+ * CONCORD_OK (0) or a negative code; concord_last_error() describes the last
+ * failure on the calling thread.  Matrices are row-major float64, p x p
+ * (n x p for data), exactly as the reference's numpy arrays.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/parconcord):
+ *   concord_gram_f64 / concord_solver_gram_from_data  -> model.compute_gram         model.py:190-197
+ *   concord_solver_fit / concord_pcd_fit               -> solver.pcd_fit            solver.py:254-294
+ *                                                         (sweeps _ckernels.pcd_sweep _ckernels.pyx:68-102,
+ *                                                          delta solver.py:287, objective model.py:210-217)
+ *   concord_solver_edge_count                          -> model.edge_count          model.py:249-253
+ *   concord_pcd_sweep_exact                            -> _ckernels.pcd_sweep       _ckernels.pyx:68-102
+ *   concord_u2_sweep_exact                             -> _ckernels.u2_sweep        _ckernels.pyx:105-118
+ *   concord_cd_sweep_exact                             -> _ckernels.cd_sweep        _ckernels.pyx:53-65
+ */
+#ifndef CONCORD_PCD_H
+#define CONCORD_PCD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CONCORD_ABI_VERSION 1
+
+/* Return codes. */
+#define CONCORD_OK 0
+#define CONCORD_ERR_ARG (-1)           /* bad dimension / argument (DimensionError, ValueError) */
+#define CONCORD_NOT_CONVERGED (-2)     /* iteration cap hit; outputs are valid (NotConverged)   */
+#define CONCORD_ERR_CUDA (-3)          /* CUDA runtime error                                    */
+#define CONCORD_ERR_ZERO_VARIANCE (-4) /* t_ii <= 0 (ZeroVarianceColumn)                        */
+#define CONCORD_ERR_NO_DEVICE (-5)     /* no CUDA device                                        */
+#define CONCORD_ERR_OOM (-6)           /* device allocation failed                              */
+
+/* Where a caller buffer lives. */
+#define CONCORD_HOST 0
+#define CONCORD_DEVICE 1
+
+typedef struct concord_solver concord_solver;
+
+typedef struct {
+    double lam;          /* penalty; the soft threshold is n*lam (solver.py:285)           */
+    double delta_tol;    /* stop when max |Omega_new - Omega_old| < delta_tol (solver.py:290) */
+    int32_t max_iter;    /* max_outer_iterations                                            */
+    int32_t want_trace;  /* 1: fused objective trace per sweep                              */
+    const double* omega_init; /* NULL = identity (model.py:158-166), else p x p warm start  */
+    int32_t init_where;  /* CONCORD_HOST / CONCORD_DEVICE for omega_init                    */
+    int32_t reserved;
+} concord_fit_params;
+
+typedef struct {
+    int32_t iterations;  /* sweeps run                                                      */
+    int32_t converged;   /* 1 if final_delta < delta_tol                                    */
+    double final_delta;  /* max |delta| of the last sweep                                   */
+    int64_t edge_count;  /* exact non-zeros of the strict upper triangle                    */
+    double kernel_ms;    /* CUDA-event time of the persistent sweep kernel                  */
+    double setup_ms;     /* CUDA-event time of W/Omega initialisation before the kernel     */
+    int32_t n_blocks;    /* CTAs (column slabs) used                                        */
+    int32_t slab_width;  /* columns per slab                                                */
+} concord_fit_result;
+
+/* ---- library / device ------------------------------------------------- */
+int concord_abi_version(void);
+const char* concord_last_error(void);
+int concord_device_count(int* count);
+
+/* ---- device-resident solver (one per problem size and device) ---------- */
+/* n_blocks: 0 = automatic slab count; otherwise the number of column slabs. */
+int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_solver** out);
+int concord_solver_destroy(concord_solver* s);
+/* Use a caller stream (cudaStream_t as void*); NULL restores the solver's own. */
+int concord_solver_set_stream(concord_solver* s, void* stream);
+void* concord_solver_stream(concord_solver* s);
+/* GramMatrix (model.py:81-103): T p x p row-major and the sample count n. */
+int concord_solver_set_gram(concord_solver* s, const double* T, double n, int32_t where);
+/* compute_gram (model.py:190-197) on the device from centred data X (n x p). */
+int concord_solver_gram_from_data(concord_solver* s, const double* X, int64_t n, int32_t where);
+int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where);
+/* pcd_fit (solver.py:254-294).  delta_trace / objective_trace / sweep_seconds
+ * may be NULL, else hold max_iter doubles.  Returns CONCORD_NOT_CONVERGED when
+ * the cap is hit (results valid, like NotConverged.report). */
+int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord_fit_result* res,
+                       double* delta_trace, double* objective_trace, double* sweep_seconds);
+int concord_solver_get_omega(concord_solver* s, double* omega_out, int32_t where);
+int concord_solver_edge_count(concord_solver* s, int64_t* out);
+/* Non-zero off-diagonal deltas of each sweep of the last fit (the row streams
+ * the kernel applied; used for the roofline's algorithmic bytes).  Copies
+ * min(cap, iterations) entries, *count = iterations of the last fit. */
+int concord_solver_sweep_stats(concord_solver* s, int64_t* nnz_pairs, int32_t cap, int32_t* count);
+
+/* ---- pinned host buffers for fast H2D/D2H of T and Omega ---------------- */
+int concord_host_alloc(int64_t bytes, void** out);
+int concord_host_free(void* ptr);
+
+/* ---- one-shot conveniences ---------------------------------------------- */
+int concord_gram_f64(const double* X, int64_t n, int64_t p, double* T_out, int32_t device);
+int concord_pcd_fit(const double* T, int64_t p, double n, const concord_fit_params* prm, double* omega_out,
+                    concord_fit_result* res, double* delta_trace, double* objective_trace,
+                    double* sweep_seconds, int32_t device);
+
+/* ---- bit-exact reference kernel protocol (host buffers, one sweep) ------- */
+/* Bitwise equal to the reference's compiled backend for the same inputs.     */
+int concord_pcd_sweep_exact(double* om, const double* t, int64_t p, double n, double shrink,
+                            const int64_t* rs, const int64_t* ss, const int64_t* offsets, int64_t nrounds,
+                            int32_t device);
+int concord_u2_sweep_exact(double* om, const double* t, int64_t p, double n, double shrink, const int64_t* rs,
+                           const int64_t* ss, int64_t npairs, int32_t device);
+int concord_cd_sweep_exact(double* om, const double* t, int64_t p, double n, double shrink, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONCORD_PCD_H */

@@ -1,0 +1,630 @@
+// extern "C" ABI of libconcord_b200.so (include/concord_pcd.h).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/concord_pcd.h"
+#include "pcd_wform.h"
+
+using namespace concord;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess) {                                                                   \
+            return fail(_e == cudaErrorMemoryAllocation ? CONCORD_ERR_OOM : CONCORD_ERR_CUDA,      \
+                        "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e));        \
+        }                                                                                          \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+cudaError_t dalloc(T** ptr, size_t count) {
+    *ptr = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc((void**)ptr, sizeof(T) * count);
+}
+
+int check_device(int32_t device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(CONCORD_ERR_NO_DEVICE, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(CONCORD_ERR_ARG, "device %d out of range [0,%d)", device, count);
+    return CONCORD_OK;
+}
+
+}  // namespace
+
+struct concord_solver {
+    int dev = 0;
+    int p = 0;
+    int w = 0;
+    int nblk = 0;
+    long long slab = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    double* T = nullptr;
+    double* W = nullptr;
+    double* Om = nullptr;
+    double* tdiag = nullptr;
+    double* stage = nullptr;  // p x p row-major scratch (lazy)
+    double2* pub = nullptr;
+    unsigned long long* bar = nullptr;
+    unsigned long long* edges = nullptr;
+    int* status = nullptr;
+    double* rec_delta = nullptr;
+    double* rec_obj = nullptr;
+    unsigned long long* rec_time = nullptr;
+    long long* rec_nnz = nullptr;
+    int rec_cap = 0;
+    int last_iters = 0;
+    int* csr_rowptr = nullptr;
+    int* csr_col = nullptr;
+    double* csr_val = nullptr;
+    long long csr_cap = 0;
+    double n = 0.0;
+    bool have_gram = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+int ensure_stage(concord_solver* s) {
+    if (!s->stage) CK(dalloc(&s->stage, (size_t)s->p * s->p));
+    return CONCORD_OK;
+}
+
+int ensure_records(concord_solver* s, int cap) {
+    if (cap <= s->rec_cap) return CONCORD_OK;
+    cudaFree(s->rec_delta);
+    cudaFree(s->rec_obj);
+    cudaFree(s->rec_time);
+    cudaFree(s->rec_nnz);
+    s->rec_delta = nullptr;
+    s->rec_obj = nullptr;
+    s->rec_time = nullptr;
+    s->rec_nnz = nullptr;
+    CK(dalloc(&s->rec_delta, cap));
+    CK(dalloc(&s->rec_nnz, cap));
+    CK(dalloc(&s->rec_obj, (size_t)cap * s->nblk * 3));
+    CK(dalloc(&s->rec_time, cap + 1));
+    s->rec_cap = cap;
+    return CONCORD_OK;
+}
+
+int finish_gram(concord_solver* s) {
+    CK(launch_slab_diag(s->T, s->tdiag, s->p, s->w, s->stream));
+    std::vector<double> d(s->p);
+    CK(cudaMemcpyAsync(d.data(), s->tdiag, sizeof(double) * s->p, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    for (int i = 0; i < s->p; ++i)
+        if (!(d[i] > 0.0)) {
+            s->have_gram = false;
+            return fail(CONCORD_ERR_ZERO_VARIANCE, "column %d has zero sum of squares", i);
+        }
+    s->have_gram = true;
+    return CONCORD_OK;
+}
+
+// Upload a row-major p x p matrix (host or device) into a slab buffer.
+int upload_slabs(concord_solver* s, const double* src, int32_t where, double* dst) {
+    const double* dsrc = src;
+    if (where == CONCORD_HOST) {
+        int rc = ensure_stage(s);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(s->stage, src, sizeof(double) * (size_t)s->p * s->p, cudaMemcpyHostToDevice,
+                           s->stream));
+        dsrc = s->stage;
+    }
+    CK(launch_pack_slabs(dsrc, s->p, dst, s->p, s->w, s->nblk, s->stream));
+    return CONCORD_OK;
+}
+
+int download_slabs(concord_solver* s, const double* src, double* out, int32_t where) {
+    if (where == CONCORD_DEVICE) {
+        CK(launch_unpack_slabs(src, out, s->p, s->w, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        return CONCORD_OK;
+    }
+    int rc = ensure_stage(s);
+    if (rc) return rc;
+    CK(launch_unpack_slabs(src, s->stage, s->p, s->w, s->stream));
+    CK(cudaMemcpyAsync(out, s->stage, sizeof(double) * (size_t)s->p * s->p, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return CONCORD_OK;
+}
+
+// Warm start: Omega slab from omega_init, W = Omega_init * T through a CSR copy.
+int init_warm(concord_solver* s, const double* om, int32_t where) {
+    const int p = s->p;
+    std::vector<double> host;
+    const double* h = om;
+    if (where == CONCORD_DEVICE) {
+        host.resize((size_t)p * p);
+        CK(cudaMemcpyAsync(host.data(), om, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        h = host.data();
+    }
+    std::vector<int> rowptr(p + 1, 0), col;
+    std::vector<double> val;
+    for (int i = 0; i < p; ++i) {
+        const double* row = h + (size_t)i * p;
+        for (int j = 0; j < p; ++j)
+            if (row[j] != 0.0) {
+                col.push_back(j);
+                val.push_back(row[j]);
+            }
+        rowptr[i + 1] = (int)col.size();
+    }
+    const long long nnz = (long long)col.size();
+    if (nnz > s->csr_cap) {
+        cudaFree(s->csr_col);
+        cudaFree(s->csr_val);
+        s->csr_col = nullptr;
+        s->csr_val = nullptr;
+        CK(dalloc(&s->csr_col, nnz));
+        CK(dalloc(&s->csr_val, nnz));
+        s->csr_cap = nnz;
+    }
+    if (!s->csr_rowptr) CK(dalloc(&s->csr_rowptr, p + 1));
+    CK(cudaMemcpyAsync(s->csr_rowptr, rowptr.data(), sizeof(int) * (p + 1), cudaMemcpyHostToDevice, s->stream));
+    if (nnz) {
+        CK(cudaMemcpyAsync(s->csr_col, col.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaMemcpyAsync(s->csr_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s->stream));
+    }
+    int rc = upload_slabs(s, h, CONCORD_HOST, s->Om);
+    if (rc) return rc;
+    CK(launch_wform_init_csr(s->csr_rowptr, s->csr_col, s->csr_val, s->T, s->W, p, s->w, s->nblk, s->stream));
+    CK(cudaStreamSynchronize(s->stream));  // host vectors go out of scope
+    return CONCORD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int concord_abi_version(void) { return CONCORD_ABI_VERSION; }
+
+const char* concord_last_error(void) { return g_err.c_str(); }
+
+int concord_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) c = 0;
+    if (count) *count = c;
+    return CONCORD_OK;
+}
+
+int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_solver** out) {
+    if (!out) return fail(CONCORD_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (p < 2) return fail(CONCORD_ERR_ARG, "T must be square with p >= 2, got p=%lld", (long long)p);
+    if (p > (1LL << 30)) return fail(CONCORD_ERR_ARG, "p=%lld too large", (long long)p);
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    const int ip = (int)p;
+    int w;
+    if (n_blocks > 0) {
+        w = (ip + n_blocks - 1) / n_blocks;
+    } else {
+        w = (ip + nsm - 1) / nsm;
+        if (w < 8) w = 8;
+    }
+    w = (w + 1) & ~1;
+    int max_blocks = 0;
+    for (;;) {
+        if (w > WFORM_THREADS) return fail(CONCORD_ERR_ARG, "p=%d needs slab width %d > %d", ip, w, WFORM_THREADS);
+        CK(wform_max_blocks(w, &max_blocks));
+        if ((ip + w - 1) / w <= max_blocks) break;
+        w += 2;
+    }
+    concord_solver* s = new concord_solver();
+    s->dev = device;
+    s->p = ip;
+    s->w = w;
+    s->nblk = (ip + w - 1) / w;
+    s->slab = (long long)ip * w;
+    const size_t tot = (size_t)s->nblk * s->slab;
+    auto cleanup = [&](int code) {
+        concord_solver_destroy(s);
+        return code;
+    };
+#define CKC(expr)                                                                                  \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess)                                                                     \
+            return cleanup(fail(_e == cudaErrorMemoryAllocation ? CONCORD_ERR_OOM : CONCORD_ERR_CUDA, \
+                                "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e))); \
+    } while (0)
+    CKC(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
+    s->stream = s->own_stream;
+    CKC(dalloc(&s->T, tot));
+    CKC(dalloc(&s->W, tot));
+    CKC(dalloc(&s->Om, tot));
+    CKC(cudaMemsetAsync(s->T, 0, sizeof(double) * tot, s->stream));
+    CKC(cudaMemsetAsync(s->W, 0, sizeof(double) * tot, s->stream));
+    CKC(cudaMemsetAsync(s->Om, 0, sizeof(double) * tot, s->stream));
+    CKC(dalloc(&s->tdiag, ip));
+    CKC(dalloc(&s->pub, 2 * (size_t)ip));
+    CKC(dalloc(&s->bar, 1));
+    CKC(dalloc(&s->edges, 1));
+    CKC(dalloc(&s->status, 2));
+    for (auto& e : s->ev) CKC(cudaEventCreate(&e));
+    CKC(cudaStreamSynchronize(s->stream));
+#undef CKC
+    *out = s;
+    return CONCORD_OK;
+}
+
+int concord_solver_destroy(concord_solver* s) {
+    if (!s) return CONCORD_OK;
+    DeviceGuard g(s->dev);
+    if (s->own_stream) cudaStreamSynchronize(s->own_stream);
+    cudaFree(s->T);
+    cudaFree(s->W);
+    cudaFree(s->Om);
+    cudaFree(s->tdiag);
+    cudaFree(s->stage);
+    cudaFree(s->pub);
+    cudaFree(s->bar);
+    cudaFree(s->edges);
+    cudaFree(s->status);
+    cudaFree(s->rec_delta);
+    cudaFree(s->rec_obj);
+    cudaFree(s->rec_time);
+    cudaFree(s->rec_nnz);
+    cudaFree(s->csr_rowptr);
+    cudaFree(s->csr_col);
+    cudaFree(s->csr_val);
+    for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    delete s;
+    return CONCORD_OK;
+}
+
+int concord_solver_set_stream(concord_solver* s, void* stream) {
+    if (!s) return fail(CONCORD_ERR_ARG, "solver is NULL");
+    s->stream = stream ? (cudaStream_t)stream : s->own_stream;
+    return CONCORD_OK;
+}
+
+void* concord_solver_stream(concord_solver* s) { return s ? (void*)s->stream : nullptr; }
+
+int concord_solver_set_gram(concord_solver* s, const double* T, double n, int32_t where) {
+    if (!s || !T) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (!(n >= 1.0)) return fail(CONCORD_ERR_ARG, "n must be at least 1");
+    DeviceGuard g(s->dev);
+    int rc = upload_slabs(s, T, where, s->T);
+    if (rc) return rc;
+    s->n = n;
+    return finish_gram(s);
+}
+
+int concord_solver_gram_from_data(concord_solver* s, const double* X, int64_t n, int32_t where) {
+    if (!s || !X) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (n < 1) return fail(CONCORD_ERR_ARG, "need at least one observation");
+    DeviceGuard g(s->dev);
+    const double* Xd = X;
+    double* tmp = nullptr;
+    if (where == CONCORD_HOST) {
+        CK(dalloc(&tmp, (size_t)n * s->p));
+        CK(cudaMemcpyAsync(tmp, X, sizeof(double) * (size_t)n * s->p, cudaMemcpyHostToDevice, s->stream));
+        Xd = tmp;
+    }
+    cudaError_t e = cudaMemsetAsync(s->T, 0, sizeof(double) * (size_t)s->nblk * s->slab, s->stream);
+    if (e == cudaSuccess) e = launch_gram_f64(Xd, n, s->p, s->p, s->T, 1, s->w, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (tmp) cudaFree(tmp);
+    CK(e);
+    s->n = (double)n;
+    return finish_gram(s);
+}
+
+int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where) {
+    if (!s || !T_out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    DeviceGuard g(s->dev);
+    return download_slabs(s, s->T, T_out, where);
+}
+
+int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord_fit_result* res,
+                       double* delta_trace, double* objective_trace, double* sweep_seconds) {
+    if (!s || !prm) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (!s->have_gram) return fail(CONCORD_ERR_ARG, "no Gram matrix set");
+    if (!(prm->lam >= 0.0)) return fail(CONCORD_ERR_ARG, "lam must be nonnegative");
+    if (!(prm->delta_tol > 0.0)) return fail(CONCORD_ERR_ARG, "delta_tol must be positive");
+    if (prm->max_iter < 1) return fail(CONCORD_ERR_ARG, "max_outer_iterations must be at least 1");
+    DeviceGuard g(s->dev);
+    int rc = ensure_records(s, prm->max_iter);
+    if (rc) return rc;
+    const size_t tot = (size_t)s->nblk * s->slab;
+
+    CK(cudaEventRecord(s->ev[0], s->stream));
+    if (prm->omega_init) {
+        rc = init_warm(s, prm->omega_init, prm->init_where);
+        if (rc) return rc;
+    } else {
+        CK(launch_slab_identity(s->Om, s->p, s->w, s->nblk, s->stream));
+        CK(cudaMemcpyAsync(s->W, s->T, sizeof(double) * tot, cudaMemcpyDeviceToDevice, s->stream));
+    }
+    CK(cudaMemsetAsync(s->bar, 0, sizeof(unsigned long long), s->stream));
+    CK(cudaEventRecord(s->ev[1], s->stream));
+
+    WformArgs a;
+    a.p = s->p;
+    const int pe = s->p + (s->p & 1);
+    a.m = pe - 1;
+    a.half = pe / 2;
+    a.w = s->w;
+    a.slab = s->slab;
+    a.W = s->W;
+    a.T = s->T;
+    a.Om = s->Om;
+    a.tdiag = s->tdiag;
+    a.pub = s->pub;
+    a.n = s->n;
+    a.shrink = s->n * prm->lam;
+    a.delta_tol = prm->delta_tol;
+    a.max_iter = prm->max_iter;
+    a.want_trace = prm->want_trace ? 1 : 0;
+    a.bar = s->bar;
+    a.rec_delta = s->rec_delta;
+    a.rec_obj = s->rec_obj;
+    a.rec_time = s->rec_time;
+    a.rec_nnz = s->rec_nnz;
+    a.status = s->status;
+    CK(launch_pcd_wform(a, s->nblk, s->stream));
+    CK(cudaEventRecord(s->ev[2], s->stream));
+    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk, s->edges, s->stream));
+
+    int status[2] = {0, 0};
+    unsigned long long edges = 0;
+    CK(cudaMemcpyAsync(status, s->status, sizeof(status), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    const int iters = status[0];
+    s->last_iters = iters;
+    std::vector<double> dl(iters > 0 ? iters : 1);
+    std::vector<unsigned long long> tm(iters + 1);
+    CK(cudaMemcpy(dl.data(), s->rec_delta, sizeof(double) * iters, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tm.data(), s->rec_time, sizeof(unsigned long long) * (iters + 1), cudaMemcpyDeviceToHost));
+    if (delta_trace)
+        for (int i = 0; i < iters; ++i) delta_trace[i] = dl[i];
+    if (sweep_seconds)
+        for (int i = 0; i < iters; ++i) sweep_seconds[i] = (double)(tm[i + 1] - tm[i]) * 1e-9;
+    if (objective_trace) {
+        if (prm->want_trace) {
+            std::vector<double> ro((size_t)iters * s->nblk * 3);
+            CK(cudaMemcpy(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost));
+            for (int i = 0; i < iters; ++i) {
+                double q = 0.0, pen = 0.0, lg = 0.0;
+                for (int b = 0; b < s->nblk; ++b) {
+                    const double* r = &ro[((size_t)i * s->nblk + b) * 3];
+                    q += r[0];
+                    pen += r[1];
+                    lg += r[2];
+                }
+                objective_trace[i] = -s->n * lg + 0.5 * q + s->n * prm->lam * pen;
+            }
+        } else {
+            for (int i = 0; i < iters; ++i) objective_trace[i] = NAN;
+        }
+    }
+    float setup_ms = 0.f, kernel_ms = 0.f;
+    CK(cudaEventElapsedTime(&setup_ms, s->ev[0], s->ev[1]));
+    CK(cudaEventElapsedTime(&kernel_ms, s->ev[1], s->ev[2]));
+    if (res) {
+        res->iterations = iters;
+        res->converged = status[1];
+        res->final_delta = iters > 0 ? dl[iters - 1] : INFINITY;
+        res->edge_count = (int64_t)edges;
+        res->kernel_ms = kernel_ms;
+        res->setup_ms = setup_ms;
+        res->n_blocks = s->nblk;
+        res->slab_width = s->w;
+    }
+    if (!status[1]) {
+        fail(CONCORD_NOT_CONVERGED, "no convergence after %d outer iterations, final delta %.3e", iters,
+             iters > 0 ? dl[iters - 1] : INFINITY);
+        return CONCORD_NOT_CONVERGED;
+    }
+    return CONCORD_OK;
+}
+
+int concord_solver_get_omega(concord_solver* s, double* omega_out, int32_t where) {
+    if (!s || !omega_out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    DeviceGuard g(s->dev);
+    return download_slabs(s, s->Om, omega_out, where);
+}
+
+int concord_solver_edge_count(concord_solver* s, int64_t* out) {
+    if (!s || !out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    DeviceGuard g(s->dev);
+    unsigned long long edges = 0;
+    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk, s->edges, s->stream));
+    CK(cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    *out = (int64_t)edges;
+    return CONCORD_OK;
+}
+
+int concord_solver_sweep_stats(concord_solver* s, int64_t* nnz_pairs, int32_t cap, int32_t* count) {
+    if (!s || !count) return fail(CONCORD_ERR_ARG, "NULL argument");
+    DeviceGuard g(s->dev);
+    const int k = s->last_iters < cap ? s->last_iters : cap;
+    if (k > 0 && nnz_pairs) CK(cudaMemcpy(nnz_pairs, s->rec_nnz, sizeof(int64_t) * k, cudaMemcpyDeviceToHost));
+    *count = s->last_iters;
+    return CONCORD_OK;
+}
+
+int concord_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return fail(CONCORD_ERR_ARG, "bad arguments");
+    *out = nullptr;
+    CK(cudaHostAlloc(out, bytes > 0 ? (size_t)bytes : 1, cudaHostAllocPortable));
+    return CONCORD_OK;
+}
+
+int concord_host_free(void* ptr) {
+    if (ptr) CK(cudaFreeHost(ptr));
+    return CONCORD_OK;
+}
+
+int concord_gram_f64(const double* X, int64_t n, int64_t p, double* T_out, int32_t device) {
+    if (!X || !T_out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (n < 1) return fail(CONCORD_ERR_ARG, "need at least one observation");
+    if (p < 2) return fail(CONCORD_ERR_ARG, "need at least two variables");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    double *Xd = nullptr, *Td = nullptr;
+    CK(dalloc(&Xd, (size_t)n * p));
+    cudaError_t e = dalloc(&Td, (size_t)p * p);
+    if (e == cudaSuccess) e = cudaMemcpy(Xd, X, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_gram_f64(Xd, n, (int)p, p, Td, 0, 0, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(T_out, Td, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost);
+    cudaFree(Xd);
+    cudaFree(Td);
+    CK(e);
+    return CONCORD_OK;
+}
+
+int concord_pcd_fit(const double* T, int64_t p, double n, const concord_fit_params* prm, double* omega_out,
+                    concord_fit_result* res, double* delta_trace, double* objective_trace,
+                    double* sweep_seconds, int32_t device) {
+    concord_solver* s = nullptr;
+    int rc = concord_solver_create(p, device, 0, &s);
+    if (rc) return rc;
+    rc = concord_solver_set_gram(s, T, n, CONCORD_HOST);
+    int fit_rc = rc;
+    if (!rc) fit_rc = concord_solver_fit(s, prm, res, delta_trace, objective_trace, sweep_seconds);
+    if ((fit_rc == CONCORD_OK || fit_rc == CONCORD_NOT_CONVERGED) && omega_out) {
+        std::string keep = g_err;
+        rc = concord_solver_get_omega(s, omega_out, CONCORD_HOST);
+        if (rc == CONCORD_OK) g_err = keep;
+        else fit_rc = rc;
+    }
+    concord_solver_destroy(s);
+    return fit_rc;
+}
+
+// ------------------------------------------------------------ exact protocol
+namespace {
+struct ExactBufs {
+    double* om = nullptr;
+    double* t = nullptr;
+    long long* rs = nullptr;
+    long long* ss = nullptr;
+    long long* off = nullptr;
+    unsigned long long* bar = nullptr;
+    ~ExactBufs() {
+        cudaFree(om);
+        cudaFree(t);
+        cudaFree(rs);
+        cudaFree(ss);
+        cudaFree(off);
+        cudaFree(bar);
+    }
+};
+
+int exact_common(ExactBufs& b, double* om, const double* t, int64_t p) {
+    const size_t bytes = sizeof(double) * (size_t)p * p;
+    CK(dalloc(&b.om, (size_t)p * p));
+    CK(dalloc(&b.t, (size_t)p * p));
+    CK(cudaMemcpy(b.om, om, bytes, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(b.t, t, bytes, cudaMemcpyHostToDevice));
+    return CONCORD_OK;
+}
+}  // namespace
+
+int concord_pcd_sweep_exact(double* om, const double* t, int64_t p, double n, double shrink,
+                            const int64_t* rs, const int64_t* ss, const int64_t* offsets, int64_t nrounds,
+                            int32_t device) {
+    if (!om || !t || !offsets || p < 1 || nrounds < 0) return fail(CONCORD_ERR_ARG, "bad arguments");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    ExactBufs b;
+    rc = exact_common(b, om, t, p);
+    if (rc) return rc;
+    const long long m = offsets[nrounds];
+    CK(dalloc(&b.rs, m));
+    CK(dalloc(&b.ss, m));
+    CK(dalloc(&b.off, nrounds + 1));
+    CK(dalloc(&b.bar, 1));
+    if (m) {
+        CK(cudaMemcpy(b.rs, rs, sizeof(long long) * m, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(b.ss, ss, sizeof(long long) * m, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(b.off, offsets, sizeof(long long) * (nrounds + 1), cudaMemcpyHostToDevice));
+    CK(launch_pcd_sweep_exact(b.om, b.t, (int)p, n, shrink, b.rs, b.ss, b.off, (int)nrounds, b.bar, nullptr));
+    CK(cudaMemcpy(om, b.om, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost));
+    return CONCORD_OK;
+}
+
+int concord_u2_sweep_exact(double* om, const double* t, int64_t p, double n, double shrink, const int64_t* rs,
+                           const int64_t* ss, int64_t npairs, int32_t device) {
+    if (!om || !t || p < 1 || npairs < 0) return fail(CONCORD_ERR_ARG, "bad arguments");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    ExactBufs b;
+    rc = exact_common(b, om, t, p);
+    if (rc) return rc;
+    CK(dalloc(&b.rs, npairs));
+    CK(dalloc(&b.ss, npairs));
+    if (npairs) {
+        CK(cudaMemcpy(b.rs, rs, sizeof(long long) * npairs, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(b.ss, ss, sizeof(long long) * npairs, cudaMemcpyHostToDevice));
+    }
+    CK(launch_u2_sweep_exact(b.om, b.t, (int)p, n, shrink, b.rs, b.ss, npairs, nullptr));
+    CK(cudaMemcpy(om, b.om, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost));
+    return CONCORD_OK;
+}
+
+int concord_cd_sweep_exact(double* om, const double* t, int64_t p, double n, double shrink, int32_t device) {
+    if (!om || !t || p < 1) return fail(CONCORD_ERR_ARG, "bad arguments");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    ExactBufs b;
+    rc = exact_common(b, om, t, p);
+    if (rc) return rc;
+    CK(launch_cd_sweep_exact(b.om, b.t, (int)p, n, shrink, nullptr));
+    CK(cudaMemcpy(om, b.om, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost));
+    return CONCORD_OK;
+}
+
+}  // extern "C"

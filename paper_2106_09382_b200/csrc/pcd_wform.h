@@ -1,0 +1,62 @@
+// Internal C++ interface of the W-form persistent kernel (not the public ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define WFORM_THREADS 1024
+#define WFORM_LIST_CAP 4096
+
+namespace concord {
+
+struct WformArgs {
+    int p;          // problem size
+    int m;          // rounds per sweep = p_even - 1
+    int half;       // pairs per round = p_even / 2
+    int w;          // slab width (columns per CTA), even
+    long long slab; // p * w doubles per slab
+    double* W;      // slab-major p x (nblk*w): W = Omega * T
+    const double* T;
+    double* Om;     // slab-major dense Omega
+    const double* tdiag;
+    double2* pub;   // 2 * p ping-pong publish buffers
+    double n;       // sample count (GramMatrix.n)
+    double shrink;  // n * lam (solver.py:285)
+    double delta_tol;
+    int max_iter;
+    int want_trace;
+    unsigned long long* bar;
+    double* rec_delta;              // [max_iter]
+    double* rec_obj;                // [max_iter][nblk][3]: <W,Om> part, sum_{i<j}|om|, sum log om_ii
+    unsigned long long* rec_time;   // [max_iter + 1] globaltimer ns
+    long long* rec_nnz;             // [max_iter] non-zero off-diagonal deltas per sweep
+    int* status;                    // [0] iterations, [1] converged
+};
+
+inline size_t wform_smem_bytes(int w) { return (size_t)WFORM_LIST_CAP * 16 + (size_t)w * sizeof(int); }
+
+cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st);
+cudaError_t wform_max_blocks(int w, int* max_blocks);
+cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk,
+                              cudaStream_t st);
+cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, cudaStream_t st);
+cudaError_t launch_slab_diag(const double* slab, double* diag, int p, int w, cudaStream_t st);
+cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, cudaStream_t st);
+cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, unsigned long long* out,
+                                   cudaStream_t st);
+cudaError_t launch_wform_init_csr(const int* rowptr, const int* colidx, const double* vals, const double* Tslab,
+                                  double* Wslab, int p, int w, int nblk, cudaStream_t st);
+
+// Exact (direct-form) reference-protocol sweeps, pcd_exact.cu.
+cudaError_t launch_pcd_sweep_exact(double* om, const double* t, int p, double n, double shrink,
+                                   const long long* rs, const long long* ss, const long long* offsets,
+                                   int nrounds, unsigned long long* bar, cudaStream_t st);
+cudaError_t launch_u2_sweep_exact(double* om, const double* t, int p, double n, double shrink,
+                                  const long long* rs, const long long* ss, long long npairs, cudaStream_t st);
+cudaError_t launch_cd_sweep_exact(double* om, const double* t, int p, double n, double shrink, cudaStream_t st);
+
+// FP64 DMMA Gram / GEMM, gram.cu.  T = X^T X (X: n x p row-major, leading dim ldx).
+// out_mode 0: row-major p x p (ld = p); 1: slab-major with width w.
+cudaError_t launch_gram_f64(const double* X, long long n, int p, long long ldx, double* out, int out_mode, int w,
+                            cudaStream_t st);
+
+}  // namespace concord

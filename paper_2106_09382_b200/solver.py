@@ -1,0 +1,455 @@
+"""The drop-in solver entry points: pcd_fit / cd_fit / FitReport on the GPU.
+
+`pcd_fit(x_or_gram, config, schedule=None, backend=None)` keeps the signature,
+arguments, return type and exceptions of the reference driver
+(/root/reference/pkg/src/parconcord/solver.py:254-294).  With the default
+backend ("cuda") the whole fit -- every colour of every sweep, the diagonal
+step, the max |delta| convergence test and the objective trace -- runs in ONE
+persistent cooperative kernel on a device-resident W = Omega*T (pcd_wform.cu).
+
+backend="cuda-exact" instead runs the reference's own driver loop over GPU
+sweeps that reproduce the compiled reference kernel bit for bit
+(pcd_exact.cu); it is the parity hook, not the fast path.  There is no CPU
+backend: without the CUDA library or a device every entry point raises.
+"""
+
+import ctypes
+import math
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .model import (
+    DataMatrix,
+    DimensionError,
+    GramMatrix,
+    PrecisionEstimate,
+    SolverConfig,
+    compute_gram,
+)
+from .schedule import (
+    IndexPair,
+    Schedule,
+    flat_circle_schedule,
+    flatten_schedule,
+    is_circle_schedule,
+    validate_schedule,
+)
+
+BACKENDS = ("cuda", "cuda-exact")
+
+
+class NotConverged(RuntimeError):
+    """Iteration cap hit; carries the partial FitReport (solver.py:46-54)."""
+
+    def __init__(self, report):
+        self.report = report
+        super().__init__(
+            f"no convergence after {report.iterations} outer iterations, "
+            f"final delta {report.final_delta:.3e}"
+        )
+
+
+class ScheduleMismatch(ValueError):
+    """Supplied schedule does not fit the problem (solver.py:57-58)."""
+
+
+class EmptyVector(ValueError):
+    """Reduction over zero elements (solver.py:61-62)."""
+
+
+@dataclass(frozen=True)
+class FitReport:
+    """Everything a fit produced (solver.py:65-80).
+
+    wall_time_per_iteration holds the device time of each sweep (all colours,
+    the diagonal step and the fused max |delta|), measured in-kernel with the
+    GPU global timer; objective bookkeeping is fused into the diagonal stream.
+    """
+
+    estimate: PrecisionEstimate
+    iterations: int
+    final_delta: float
+    converged: bool
+    objective_trace: tuple
+    edge_count: int
+    wall_time_per_iteration: tuple
+
+
+# ----------------------------------------------------------------- backends
+
+
+def available_backends():
+    """Backends usable in this process (the CUDA library loads and a device is visible)."""
+    try:
+        _lib.load()
+        return BACKENDS if _lib.device_count() > 0 else ()
+    except Exception:
+        return ()
+
+
+def default_backend_name():
+    env = os.environ.get("CONCORD_B200_BACKEND")
+    if env:
+        if env not in BACKENDS:
+            raise ValueError(f"CONCORD_B200_BACKEND must be one of {BACKENDS}, got {env!r}")
+        return env
+    return "cuda"
+
+
+def get_backend(name=None):
+    """Sweep-level kernel module in the reference protocol (_backend.py:36-49).
+
+    Both names resolve to the bit-exact GPU sweeps (`name`, `cd_sweep`,
+    `pcd_sweep`, `u2_sweep`), so the reference's own driver loop and tests run
+    against the GPU unchanged.
+    """
+    if name is None:
+        name = default_backend_name()
+    if name not in BACKENDS:
+        raise ValueError(f"unknown backend {name!r}")
+    from . import cuda_kernels
+
+    _lib.require_device()
+    return cuda_kernels
+
+
+# ----------------------------------------------------------- host utilities
+
+
+def cyclic_max_reduce(d) -> float:
+    """max |d_j| (solver.py:141-163); the device fuses this into the sweep."""
+    work = np.asarray(d, dtype=np.float64).ravel()
+    if work.size == 0:
+        raise EmptyVector("cannot reduce an empty vector")
+    return float(np.max(np.abs(work)))
+
+
+def diff_vector(a: PrecisionEstimate, b: PrecisionEstimate):
+    """Stacked upper-triangle difference, length p(p+1)/2 (solver.py:192-200)."""
+    if a.p != b.p:
+        raise DimensionError(f"shapes differ: p={a.p} vs p={b.p}")
+    iu = np.triu_indices(a.p)
+    return (a.omega - b.omega)[iu]
+
+
+def _as_gram(x_or_gram, device=0):
+    if isinstance(x_or_gram, GramMatrix):
+        return x_or_gram
+    if isinstance(x_or_gram, DataMatrix):
+        return compute_gram(x_or_gram, device=device)
+    raise TypeError("expected a DataMatrix or GramMatrix")
+
+
+# ------------------------------------------------------- device-resident solver
+
+
+class Solver:
+    """A device-resident CONCORD-PCD problem of size p on one GPU.
+
+    Holds T, W = Omega*T and Omega in column-slab layout in HBM.  Use it to
+    keep T resident across many fits (e.g. a lambda path); `pcd_fit` uses a
+    transient one.
+    """
+
+    def __init__(self, p, device=0, n_blocks=0):
+        L = _lib.load()
+        _lib.require_device()
+        h = ctypes.c_void_p()
+        _lib.check(L.concord_solver_create(int(p), int(device), int(n_blocks), ctypes.byref(h)))
+        self._h = h
+        self.p = int(p)
+        self.device = int(device)
+        self.n = None
+        self.last_result = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().concord_solver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_stream(self, stream_ptr):
+        _lib.check(_lib.load().concord_solver_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))
+
+    def set_gram(self, gram: GramMatrix):
+        if gram.p != self.p:
+            raise DimensionError(f"solver has p={self.p} but gram has p={gram.p}")
+        t = np.ascontiguousarray(gram.t, dtype=np.float64)
+        _lib.check(_lib.load().concord_solver_set_gram(self._h, _lib.ptr(t), float(gram.n), _lib.HOST))
+        self.n = gram.n
+
+    def set_gram_device(self, t_dev_ptr, n):
+        """T already in device memory (row-major p x p float64 at t_dev_ptr)."""
+        _lib.check(_lib.load().concord_solver_set_gram(self._h, ctypes.c_void_p(t_dev_ptr), float(n),
+                                                      _lib.DEVICE))
+        self.n = n
+
+    def gram_from_data(self, x: DataMatrix):
+        if x.p != self.p:
+            raise DimensionError(f"solver has p={self.p} but data has p={x.p}")
+        _lib.check(_lib.load().concord_solver_gram_from_data(self._h, _lib.ptr(x.values), x.n, _lib.HOST))
+        self.n = x.n
+
+    def gram(self) -> GramMatrix:
+        t = np.empty((self.p, self.p))
+        _lib.check(_lib.load().concord_solver_get_gram(self._h, _lib.ptr(t), _lib.HOST))
+        return GramMatrix._trusted(t, self.n)
+
+    def fit_raw(self, lam, delta_tol=1e-5, max_iter=200, init=None, trace=True):
+        """Run the persistent fit; returns (code, FitResult, deltas, objectives, sweep_seconds)."""
+        L = _lib.load()
+        prm = _lib.FitParams()
+        prm.lam = float(lam)
+        prm.delta_tol = float(delta_tol)
+        prm.max_iter = int(max_iter)
+        prm.want_trace = 1 if trace else 0
+        keep = None
+        if init is not None:
+            keep = np.ascontiguousarray(init, dtype=np.float64)
+            if keep.shape != (self.p, self.p):
+                raise DimensionError(f"init has p={keep.shape[0]} but the problem has p={self.p}")
+            prm.omega_init = keep.ctypes.data
+            prm.init_where = _lib.HOST
+        res = _lib.FitResult()
+        deltas = np.zeros(max_iter)
+        objs = np.zeros(max_iter)
+        secs = np.zeros(max_iter)
+        rc = L.concord_solver_fit(self._h, ctypes.byref(prm), ctypes.byref(res), _lib.ptr(deltas),
+                                  _lib.ptr(objs), _lib.ptr(secs))
+        _lib.check(rc, allow=(_lib.CONCORD_NOT_CONVERGED,))
+        self.last_result = res
+        k = res.iterations
+        return rc, res, deltas[:k], objs[:k], secs[:k]
+
+    def omega(self, out=None):
+        if out is None:
+            out = np.empty((self.p, self.p))
+        _lib.check(_lib.load().concord_solver_get_omega(self._h, _lib.ptr(out), _lib.HOST))
+        return out
+
+    def fit(self, lam, delta_tol=1e-5, max_iter=200, init=None, trace=True, raise_on_cap=True) -> FitReport:
+        rc, res, deltas, objs, secs = self.fit_raw(lam, delta_tol, max_iter, init, trace)
+        om = self.omega()
+        report = FitReport(
+            estimate=PrecisionEstimate._trusted(om),
+            iterations=int(res.iterations),
+            final_delta=float(res.final_delta),
+            converged=bool(res.converged),
+            objective_trace=tuple(float(v) for v in objs) if trace else (),
+            edge_count=int(res.edge_count),
+            wall_time_per_iteration=tuple(float(v) for v in secs),
+        )
+        if rc == _lib.CONCORD_NOT_CONVERGED and raise_on_cap:
+            raise NotConverged(report)
+        return report
+
+
+def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_start=False, device=0,
+             trace=True):
+    """Fit a lambda path with T resident on the device.
+
+    Cold mode (default) fits every lambda from the identity, exactly like
+    independent `pcd_fit` calls; warm mode starts each fit from the previous
+    estimate (SolverConfig.init semantics).  Returns one FitReport per lambda
+    (a non-converged fit is returned with converged=False, not raised).
+    """
+    with Solver(_gram_p(x_or_gram), device=device) as s:
+        if isinstance(x_or_gram, DataMatrix):
+            s.gram_from_data(x_or_gram)
+        elif isinstance(x_or_gram, GramMatrix):
+            s.set_gram(x_or_gram)
+        else:
+            raise TypeError("expected a DataMatrix or GramMatrix")
+        reports, prev = [], None
+        for lam in lams:
+            rep = s.fit(lam, delta_tol, max_outer_iterations, init=prev if warm_start else None, trace=trace,
+                        raise_on_cap=False)
+            reports.append(rep)
+            prev = rep.estimate.omega
+        return reports
+
+
+def _gram_p(x):
+    if isinstance(x, (GramMatrix, DataMatrix)):
+        return x.p
+    raise TypeError("expected a DataMatrix or GramMatrix")
+
+
+# Device buffers are reused across pcd_fit calls of the same size and device
+# (allocation of 4 x 8p^2 bytes per call would otherwise dominate small fits).
+_POOL = {}
+
+
+def _pooled_solver(p, device):
+    key = (int(p), int(device))
+    s = _POOL.get(key)
+    if s is None or s._h is None:
+        if len(_POOL) >= 2:
+            release_device_memory()
+        s = Solver(p, device=device)
+        _POOL[key] = s
+    return s
+
+
+def release_device_memory():
+    """Free the device buffers pcd_fit keeps for reuse."""
+    for s in list(_POOL.values()):
+        s.close()
+    _POOL.clear()
+
+
+# --------------------------------------------------------------- the drivers
+
+
+def _schedule_arrays(schedule, p):
+    if schedule is None:
+        return None
+    if schedule.p != p:
+        raise ScheduleMismatch(f"schedule is for p={schedule.p} but the problem has p={p}")
+    rep = validate_schedule(schedule)
+    if not rep.ok:
+        raise ScheduleMismatch(f"invalid schedule: {rep.message}")
+    if is_circle_schedule(schedule):
+        return None
+    return flatten_schedule(schedule)
+
+
+def pcd_fit(x_or_gram, config: SolverConfig, schedule: Schedule = None, backend=None,
+            device: int = 0) -> FitReport:
+    """Parallel coordinate descent over the circle schedule (solver.py:254-294).
+
+    Raises NotConverged (carrying the partial report) when
+    config.max_outer_iterations is exhausted first.
+    """
+    name = default_backend_name() if backend is None else backend
+    if name not in BACKENDS:
+        raise ValueError(f"unknown backend {name!r}")
+    gram = _as_gram(x_or_gram, device)
+    p = gram.p
+    custom = _schedule_arrays(schedule, p)
+    init = None if isinstance(config.init, str) else config.init
+    if init is not None and init.p != p:
+        raise DimensionError(f"init has p={init.p} but the problem has p={p}")
+    if name == "cuda" and custom is None:
+        s = _pooled_solver(p, device)
+        s.set_gram(gram)
+        return s.fit(config.lam, config.delta_tol, config.max_outer_iterations,
+                     init=None if init is None else init.omega, trace=True)
+    # Reference driver loop over the bit-exact GPU sweeps (also any non-circle schedule).
+    from . import cuda_kernels
+
+    rs, ss, offsets = custom if custom is not None else flat_circle_schedule(p)
+    return _host_loop(gram, config, lambda om, t, n, shrink: cuda_kernels.pcd_sweep(
+        om, t, n, shrink, rs, ss, offsets, config.workers, device=device), max_abs_vech=True)
+
+
+def cd_fit(x_or_gram, config: SolverConfig, backend=None, device: int = 0) -> FitReport:
+    """Serial cyclic coordinate descent (solver.py:227-251) on exact GPU sweeps.
+
+    Kept for API completeness; it is inherently serial (one pair at a time) and
+    meant for small p.
+    """
+    name = default_backend_name() if backend is None else backend
+    if name not in BACKENDS:
+        raise ValueError(f"unknown backend {name!r}")
+    gram = _as_gram(x_or_gram, device)
+    from . import cuda_kernels
+
+    return _host_loop(gram, config, lambda om, t, n, shrink: cuda_kernels.cd_sweep(om, t, n, shrink,
+                                                                                   device=device),
+                      max_abs_vech=False)
+
+
+def _objective_host(om, t, n, lam):
+    from .model import objective
+
+    return objective(PrecisionEstimate._trusted(om), GramMatrix._trusted(t, n), lam)
+
+
+def _host_loop(gram, config, sweep, max_abs_vech):
+    t, n, p = gram.t, float(gram.n), gram.p
+    omega = config.initial_omega(p)
+    trace, times = [], []
+    delta = math.inf
+    iu = np.triu_indices(p) if max_abs_vech else None
+    for it in range(1, config.max_outer_iterations + 1):
+        snapshot = omega.copy()
+        tic = time.perf_counter()
+        sweep(omega, t, n, n * config.lam)
+        diff = omega - snapshot
+        delta = float(np.max(np.abs(diff[iu] if iu is not None else diff)))
+        times.append(time.perf_counter() - tic)
+        trace.append(_objective_host(omega, t, n, config.lam))
+        if delta < config.delta_tol:
+            return _finish(omega, it, delta, True, trace, times)
+    raise NotConverged(_finish(omega, config.max_outer_iterations, delta, False, trace, times))
+
+
+def _finish(omega, iterations, delta, converged, trace, times):
+    est = PrecisionEstimate(omega)
+    return FitReport(
+        estimate=est,
+        iterations=iterations,
+        final_delta=delta,
+        converged=converged,
+        objective_trace=tuple(trace),
+        edge_count=int(np.count_nonzero(np.triu(omega, 1))),
+        wall_time_per_iteration=tuple(times),
+    )
+
+
+# ----------------------------------------------- scalar inspectors (API parity)
+
+
+def update_offdiagonal(estimate: PrecisionEstimate, gram: GramMatrix, r: int, s: int, lam: float) -> float:
+    """New value of pair (r, s), 0-based, without mutating (solver.py:86-109)."""
+    p = estimate.p
+    if not (0 <= r < p and 0 <= s < p):
+        raise IndexError(f"indices ({r}, {s}) out of range for p={p}")
+    if r == s:
+        raise ValueError("off-diagonal update needs r != s")
+    if estimate.p != gram.p:
+        raise DimensionError("estimate and gram sizes differ")
+    om, t = estimate.omega, gram.t
+    s1 = float(np.dot(om[r], t[s]))
+    s2 = float(np.dot(om[s], t[r]))
+    num = -(s1 + s2 - om[r, s] * (t[s, s] + t[r, r]))
+    from .model import soft_threshold
+
+    return soft_threshold(num, float(gram.n) * lam) / (t[r, r] + t[s, s])
+
+
+def update_diagonal(estimate: PrecisionEstimate, gram: GramMatrix, i: int) -> float:
+    """New value of diagonal entry i, 0-based, without mutating (solver.py:112-118)."""
+    p = estimate.p
+    if not 0 <= i < p:
+        raise IndexError(f"index {i} out of range for p={p}")
+    if estimate.p != gram.p:
+        raise DimensionError("estimate and gram sizes differ")
+    om, t = estimate.omega, gram.t
+    a = float(np.dot(om[i], t[i])) - om[i, i] * t[i, i]
+    return (-a + math.sqrt(a * a + 4.0 * gram.n * t[i, i])) / (2.0 * t[i, i])
+
+
+def read_write_sets(p: int, pair: IndexPair):
+    """Cells a pair update reads and writes, 1-based (solver.py:124-138)."""
+    r, s = pair.r, pair.s
+    if not (1 <= r < s <= p):
+        raise IndexError(f"pair ({r}, {s}) out of range for p={p}")
+    read = {(r, u) for u in range(1, p + 1) if u != s} | {(u, s) for u in range(1, p + 1) if u != r}
+    return read, {(r, s), (s, r)}

@@ -1,0 +1,97 @@
+"""Synthetic CONCORD problems (host side; input generation for tests and bench).
+
+Follows /root/reference/pkg/src/parconcord/datagen.py so that the same seeds
+give the same matrices as the reference's generators (checked bitwise against
+the reference in tests/golden/make_golden.py).  Not on the hot path.
+"""
+
+import numpy as np
+from scipy.linalg import solve_triangular
+
+MAX_HUB_DEGREE = 40  # datagen.py:37
+
+
+class NotPositiveDefinite(ValueError):
+    """datagen.py:32."""
+
+
+def ar2_precision(p):
+    """datagen.py:64-78: unit diagonal, first band 0.45, second band 0.40."""
+    if p < 3:
+        raise ValueError("ar2 truth needs p >= 3")
+    om = np.eye(p)
+    i = np.arange(p - 1)
+    om[i, i + 1] = om[i + 1, i] = 0.45
+    i = np.arange(p - 2)
+    om[i, i + 2] = om[i + 2, i] = 0.40
+    return om
+
+
+def _attachment_edges(p, alpha, rng):
+    """datagen.py:81-96."""
+    a0 = alpha - 3.0
+    deg = np.zeros(p)
+    edges = [(0, 1)]
+    deg[0] = deg[1] = 1.0
+    for v in range(2, p):
+        w = deg[:v] + a0
+        w[deg[:v] >= MAX_HUB_DEGREE] = 0.0
+        cum = np.cumsum(w)
+        u = int(np.searchsorted(cum, rng.random() * cum[-1], side="right"))
+        edges.append((u, v))
+        deg[u] += 1.0
+        deg[v] += 1.0
+    return edges
+
+
+def scale_free_precision(p, alpha=2.3, seed=0):
+    """datagen.py:99-132."""
+    if p < 3:
+        raise ValueError("scale-free truth needs p >= 3")
+    graph_seed, weight_seed = np.random.SeedSequence(seed).spawn(2)
+    rng_graph = np.random.default_rng(graph_seed)
+    rng_weight = np.random.default_rng(weight_seed)
+    edges = _attachment_edges(p, alpha, rng_graph)
+    u = np.zeros((p, p))
+    mags = rng_weight.uniform(0.5, 1.0, size=len(edges))
+    signs = rng_weight.choice([-1.0, 1.0], size=len(edges))
+    for (i, j), m, s in zip(edges, mags, signs):
+        u[i, j] = u[j, i] = m * s
+    r = np.abs(u).sum(axis=1)
+    b = u / (1.25 * np.sqrt(np.outer(r, r)))
+    b = 0.5 * (b + b.T)
+    support = u != 0.0
+    small = support & (np.abs(b) < 0.1)
+    b[small] = 0.1 * np.sign(b[small])
+    np.fill_diagonal(b, 1.0)
+    return b
+
+
+def sample_mvn(omega_true, n, seed=0):
+    """datagen.py:135-154: n rows of N(0, inv(omega_true)), raw (uncentered)."""
+    try:
+        chol = np.linalg.cholesky(omega_true)
+    except np.linalg.LinAlgError as exc:
+        raise NotPositiveDefinite("truth is not positive definite") from exc
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((n, omega_true.shape[0]))
+    x = solve_triangular(chol, z.T, lower=True, trans="T").T
+    return np.ascontiguousarray(x)
+
+
+def center(x):
+    """model.py:182-187 (center_columns on a raw array)."""
+    return x - x.mean(axis=0)
+
+
+def host_gram(x):
+    """model.py:190-197 on the host: 0.5*(X^T X + (X^T X)^T)."""
+    raw = x.T @ x
+    return 0.5 * (raw + raw.T)
+
+
+def problem(kind, p, n, seed=0):
+    """(centered X, T) for a truth kind in {"ar2", "scale_free"}."""
+    truth = ar2_precision(p) if kind == "ar2" else scale_free_precision(p, seed=seed)
+    x = center(sample_mvn(truth, n, seed=seed))
+    return x, host_gram(x)

@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path against the reference (golden vectors) and the oracle.
+
+Tolerances (north star: "Omega within a stated relative tolerance, e.g. 1e-8
+in FP64", identical sparsity and schedule):
+  * exact sweeps (backend "cuda-exact", pcd_exact.cu): BITWISE equal;
+  * W-form fit (default backend, pcd_wform.cu): max |dOmega| <= 1e-9 * max |Omega|,
+    identical support, edge count and iteration count; objective trace rtol 1e-10.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2106_09382_b200 as cb
+from paper_2106_09382_b200 import cuda_kernels, synth
+from conftest import case
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-9
+FIT_CASES = ["ar2_p100_n50_l0.3", "ar2_p100_n50_l0.1", "ar2_p100_n50_l0.3_tol1e-8", "sf_p101_n50_l0.3",
+             "ar2_p9_n70_l0.1", "ar2_p12_n60_l0.1_tol1e-8"]
+
+
+def assert_close_support(got, want, rel=REL_TOL):
+    scale = np.max(np.abs(want))
+    err = np.max(np.abs(got - want))
+    assert err <= rel * scale, f"max abs diff {err:.3e} > {rel:.0e} * {scale:.3e}"
+    assert np.array_equal(got != 0.0, want != 0.0), "support differs"
+    assert np.array_equal(got, got.T), "not exactly symmetric"
+
+
+# ------------------------------------------------------------ exact sweeps
+
+
+@pytest.mark.parametrize("name", ["ar2_p100_n50_l0.3", "sf_p101_n50_l0.3", "ar2_p9_n70_l0.1"])
+def test_exact_sweeps_bitwise_equal_reference(golden, name):
+    c = case(golden, name)
+    rs, ss, off = cb.flat_circle_schedule(c["p"])
+    om = np.eye(c["p"])
+    for k in range(3):
+        cuda_kernels.pcd_sweep(om, c["t"], c["n"], c["n"] * c["lam"], rs, ss, off, 1)
+        assert np.array_equal(om, golden[f"{name}_sweep{k + 1}"]), k
+
+
+def test_exact_u2_equals_pcd_and_cd_matches_reference(golden):
+    c = case(golden, "ar2_p9_n70_l0.1")
+    rs, ss, off = cb.flat_circle_schedule(9)
+    a, b = np.eye(9), np.eye(9)
+    for _ in range(3):
+        cuda_kernels.pcd_sweep(a, c["t"], c["n"], c["n"] * 0.1, rs, ss, off, 1)
+        cuda_kernels.u2_sweep(b, c["t"], c["n"], c["n"] * 0.1, rs, ss)
+        assert np.array_equal(a, b)
+    rep = cb.cd_fit(cb.GramMatrix(c["t"], c["n"]), cb.SolverConfig(lam=c["lam"], delta_tol=c["tol"],
+                                                                    max_outer_iterations=5000))
+    assert rep.iterations == c["cd_iters"]
+    assert np.array_equal(rep.estimate.omega, c["cd_omega"])
+
+
+@pytest.mark.parametrize("name", ["ar2_p100_n50_l0.3", "sf_p101_n50_l0.3", "ar2_p12_n60_l0.1_tol1e-8"])
+def test_exact_backend_fit_bitwise_equal_reference(golden, name):
+    c = case(golden, name)
+    cfg = cb.SolverConfig(lam=c["lam"], delta_tol=c["tol"], max_outer_iterations=5000)
+    rep = cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cfg, backend="cuda-exact")
+    assert rep.iterations == c["iters"]
+    assert np.array_equal(rep.estimate.omega, c["omega"])
+    assert rep.final_delta == c["delta"]
+
+
+def test_exact_protocol_rejects_bad_buffers():
+    t = np.eye(4)
+    rs, ss, off = cb.flat_circle_schedule(4)
+    with pytest.raises(ValueError):
+        cuda_kernels.pcd_sweep(np.eye(4, dtype=np.float32), t, 10, 1.0, rs, ss, off, 1)
+    with pytest.raises(ValueError):
+        cuda_kernels.pcd_sweep(np.asfortranarray(np.eye(4) + 0.5), t, 10, 1.0, rs, ss, off, 1)
+
+
+# ---------------------------------------------------------- W-form fit
+
+
+@pytest.mark.parametrize("name", FIT_CASES)
+def test_wform_fit_matches_reference(golden, name):
+    c = case(golden, name)
+    cfg = cb.SolverConfig(lam=c["lam"], delta_tol=c["tol"], max_outer_iterations=5000)
+    rep = cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cfg)
+    assert rep.iterations == c["iters"]
+    assert rep.edge_count == c["edges"]
+    assert rep.converged and rep.final_delta < c["tol"]
+    assert_close_support(rep.estimate.omega, c["omega"])
+    np.testing.assert_allclose(rep.objective_trace, c["obj"], rtol=1e-10)
+    assert len(rep.wall_time_per_iteration) == rep.iterations
+    assert all(t > 0 for t in rep.wall_time_per_iteration)
+
+
+@pytest.mark.parametrize("kind,p", [("scale_free", 1000), ("scale_free", 1001), ("ar2", 1000)])
+def test_wform_config2_matches_oracle(oracle, kind, p):
+    _, t = synth.problem(kind, p, 500, seed=0)
+    ref = oracle.pcd_fit(t, 500, 0.3, 1e-5, 5000, workers=8, trace=False)
+    rep = cb.pcd_fit(cb.GramMatrix(t, 500), cb.SolverConfig(lam=0.3, max_outer_iterations=5000))
+    assert rep.iterations == ref["iterations"]
+    assert rep.edge_count == ref["edge_count"]
+    assert_close_support(rep.estimate.omega, ref["omega"])
+
+
+@pytest.mark.parametrize("p,lam", [(2, 0.1), (3, 0.05), (5, 0.0), (64, 0.0), (257, 0.2)])
+def test_wform_edge_cases_match_oracle(oracle, p, lam):
+    rng = np.random.default_rng(p)
+    x = rng.standard_normal((3 * p + 2, p))
+    x -= x.mean(axis=0)
+    t = synth.host_gram(x)
+    n = x.shape[0]
+    ref = oracle.pcd_fit(t, n, lam, 1e-7, 20000, trace=True)
+    rep = cb.pcd_fit(cb.GramMatrix(t, n), cb.SolverConfig(lam=lam, delta_tol=1e-7, max_outer_iterations=20000))
+    assert rep.iterations == ref["iterations"]
+    assert_close_support(rep.estimate.omega, ref["omega"], rel=1e-8)
+    np.testing.assert_allclose(rep.objective_trace, ref["objective_trace"], rtol=1e-9)
+
+
+def test_wform_one_sweep_at_p2000_matches_oracle(oracle):
+    """Dense-ish first sweep at a size where rows no longer fit one slab."""
+    _, t = synth.problem("ar2", 2000, 1000, seed=1)
+    om = np.eye(2000)
+    rs, ss, off = oracle.circle_flat(2000)
+    oracle.pcd_sweep(om, t, 1000, 1000 * 0.1, rs, ss, off, 8)
+    with cb.Solver(2000) as s:
+        s.set_gram(cb.GramMatrix(t, 1000))
+        rc, res, deltas, objs, secs = s.fit_raw(0.1, 1e-5, 1)
+        got = s.omega()
+    assert res.iterations == 1
+    assert_close_support(got, om)
+
+
+def test_slab_count_never_changes_bits(golden):
+    """GPU analogue of worker invariance (test_solver.py:222-230)."""
+    c = case(golden, "ar2_p100_n50_l0.1")
+    outs = []
+    for nb in (0, 1, 3, 7, 50):
+        with cb.Solver(100, n_blocks=nb) as s:
+            s.set_gram(cb.GramMatrix(c["t"], c["n"]))
+            rep = s.fit(c["lam"], c["tol"], 5000)
+        outs.append(rep)
+    for r in outs[1:]:
+        assert np.array_equal(r.estimate.omega, outs[0].estimate.omega)
+        assert r.iterations == outs[0].iterations
+
+
+def test_fit_is_deterministic_and_data_path_equals_gram_path(golden):
+    c = case(golden, "sf_p101_n50_l0.3")
+    cfg = cb.SolverConfig(lam=0.3)
+    dm = cb.DataMatrix(c["x"], centered=True)
+    a = cb.pcd_fit(dm, cfg)
+    b = cb.pcd_fit(cb.compute_gram(dm), cfg)
+    assert np.array_equal(a.estimate.omega, b.estimate.omega)
+    assert a.objective_trace == b.objective_trace
+
+
+def test_device_gram_matches_host(golden):
+    rng = np.random.default_rng(3)
+    for n, p in ((50, 100), (37, 129), (500, 1000), (7, 65)):
+        x = rng.standard_normal((n, p))
+        g = cb.compute_gram(cb.DataMatrix(x))
+        assert np.array_equal(g.t, g.t.T)
+        want = x.T @ x
+        np.testing.assert_allclose(g.t, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+    g2 = cb.compute_gram(cb.DataMatrix(np.array([[1.0, 2.0], [3.0, 4.0]])))
+    assert np.array_equal(g2.t, golden["gram_2x2"])
+
+
+def test_not_converged_carries_partial_report(golden):
+    c = case(golden, "ar2_p100_n50_l0.1")
+    with pytest.raises(cb.NotConverged) as err:
+        cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cb.SolverConfig(lam=0.1, max_outer_iterations=2))
+    rep = err.value.report
+    assert not rep.converged and rep.iterations == 2 and rep.final_delta >= 1e-5
+    assert isinstance(rep.estimate, cb.PrecisionEstimate)
+
+
+def test_huge_lambda_gives_diagonal_fixed_point(golden):
+    c = case(golden, "ar2_p100_n50_l0.3")
+    rep = cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cb.SolverConfig(lam=1e6, delta_tol=1e-8))
+    assert rep.edge_count == 0
+    np.testing.assert_allclose(np.diag(rep.estimate.omega), np.sqrt(c["n"] / np.diag(c["t"])), rtol=1e-12)
+
+
+def test_warm_start_matches_oracle(oracle, golden):
+    c = case(golden, "ar2_p100_n50_l0.3")
+    init = golden["ar2_p100_n50_l0.1_omega"]
+    ref = oracle.pcd_fit(c["t"], c["n"], 0.3, 1e-6, 5000, init=init)
+    cfg = cb.SolverConfig(lam=0.3, delta_tol=1e-6, max_outer_iterations=5000, init=cb.PrecisionEstimate(init))
+    rep = cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cfg)
+    assert rep.iterations == ref["iterations"]
+    assert_close_support(rep.estimate.omega, ref["omega"], rel=1e-8)
+
+
+def test_lambda_path_cold_equals_independent_fits(golden):
+    c = case(golden, "ar2_p100_n50_l0.3")
+    g = cb.GramMatrix(c["t"], c["n"])
+    lams = [0.5, 0.3, 0.2]
+    path = cb.pcd_path(g, lams, delta_tol=1e-6, max_outer_iterations=5000)
+    for lam, rep in zip(lams, path):
+        one = cb.pcd_fit(g, cb.SolverConfig(lam=lam, delta_tol=1e-6, max_outer_iterations=5000))
+        assert np.array_equal(rep.estimate.omega, one.estimate.omega)
+    warm = cb.pcd_path(g, lams, delta_tol=1e-6, max_outer_iterations=5000, warm_start=True)
+    for a, b in zip(warm, path):
+        assert a.converged and np.max(np.abs(a.estimate.omega - b.estimate.omega)) < 1e-3
+
+
+def test_custom_schedule_runs_bitwise_like_reference(oracle, golden):
+    c = case(golden, "ar2_p9_n70_l0.1")
+    import dataclasses
+
+    sched = cb.build_circle_schedule(9)
+    rev = dataclasses.replace(sched, rounds=sched.rounds[::-1])
+    cfg = cb.SolverConfig(lam=0.1, delta_tol=1e-6)
+    rep = cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cfg, schedule=rev)
+    from paper_2106_09382_b200.schedule import flatten_schedule
+
+    rs, ss, off = flatten_schedule(rev)
+    om = np.eye(9)
+    for _ in range(rep.iterations):
+        oracle.pcd_sweep(om, c["t"], c["n"], c["n"] * 0.1, rs, ss, off, 1)
+    assert np.array_equal(rep.estimate.omega, om)
+    with pytest.raises(cb.ScheduleMismatch):
+        cb.pcd_fit(cb.GramMatrix(c["t"], c["n"]), cfg, schedule=cb.build_circle_schedule(5))
+
+
+def test_objective_monotone_large_p():
+    _, t = synth.problem("ar2", 3000, 1500, seed=2)
+    rep = cb.pcd_fit(cb.GramMatrix(t, 1500), cb.SolverConfig(lam=0.2, max_outer_iterations=500))
+    tr = rep.objective_trace
+    assert all(b <= a + 1e-9 * abs(a) for a, b in zip(tr, tr[1:]))
+    om = rep.estimate.omega
+    assert np.array_equal(om, om.T) and np.all(np.diag(om) > 0)
