@@ -1,6 +1,7 @@
 // extern "C" ABI of libconcord_b200.so (include/concord_pcd.h).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -86,7 +87,12 @@ struct concord_solver {
     double* rec_obj = nullptr;
     unsigned long long* rec_time = nullptr;
     long long* rec_nnz = nullptr;
+    unsigned long long* rec_dmax = nullptr;
     int rec_cap = 0;
+    int share = 0;
+    int2* list_rs = nullptr;
+    double2* list_dn = nullptr;
+    int* list_cnt = nullptr;
     int last_iters = 0;
     int* csr_rowptr = nullptr;
     int* csr_col = nullptr;
@@ -110,12 +116,15 @@ int ensure_records(concord_solver* s, int cap) {
     cudaFree(s->rec_obj);
     cudaFree(s->rec_time);
     cudaFree(s->rec_nnz);
+    cudaFree(s->rec_dmax);
+    s->rec_dmax = nullptr;
     s->rec_delta = nullptr;
     s->rec_obj = nullptr;
     s->rec_time = nullptr;
     s->rec_nnz = nullptr;
     CK(dalloc(&s->rec_delta, cap));
     CK(dalloc(&s->rec_nnz, cap));
+    CK(dalloc(&s->rec_dmax, cap));
     CK(dalloc(&s->rec_obj, (size_t)cap * s->nblk * 3));
     CK(dalloc(&s->rec_time, cap + 1));
     s->rec_cap = cap;
@@ -248,7 +257,7 @@ int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_s
     for (;;) {
         if (w > WFORM_THREADS) return fail(CONCORD_ERR_ARG, "p=%d needs slab width %d > %d", ip, w, WFORM_THREADS);
         CK(wform_max_blocks(w, &max_blocks));
-        if ((ip + w - 1) / w <= max_blocks) break;
+        if ((ip + w - 1) / w <= max_blocks && (ip + w - 1) / w <= WFORM_MAX_BLOCKS) break;
         w += 2;
     }
     concord_solver* s = new concord_solver();
@@ -278,7 +287,15 @@ int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_s
     CKC(cudaMemsetAsync(s->W, 0, sizeof(double) * tot, s->stream));
     CKC(cudaMemsetAsync(s->Om, 0, sizeof(double) * tot, s->stream));
     CKC(dalloc(&s->tdiag, ip));
-    CKC(dalloc(&s->pub, 2 * (size_t)ip));
+    CKC(dalloc(&s->pub, 3 * (size_t)ip));
+    {
+        const int half = (ip + (ip & 1)) / 2;
+        s->share = (half + s->nblk - 1) / s->nblk;
+        const size_t entries = 3 * (size_t)s->nblk * s->share;
+        CKC(dalloc(&s->list_rs, entries));
+        CKC(dalloc(&s->list_dn, entries));
+        CKC(dalloc(&s->list_cnt, 3 * (size_t)s->nblk));
+    }
     CKC(dalloc(&s->bar, 1));
     CKC(dalloc(&s->edges, 1));
     CKC(dalloc(&s->status, 2));
@@ -306,6 +323,10 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->rec_obj);
     cudaFree(s->rec_time);
     cudaFree(s->rec_nnz);
+    cudaFree(s->rec_dmax);
+    cudaFree(s->list_rs);
+    cudaFree(s->list_dn);
+    cudaFree(s->list_cnt);
     cudaFree(s->csr_rowptr);
     cudaFree(s->csr_col);
     cudaFree(s->csr_val);
@@ -381,6 +402,8 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         CK(cudaMemcpyAsync(s->W, s->T, sizeof(double) * tot, cudaMemcpyDeviceToDevice, s->stream));
     }
     CK(cudaMemsetAsync(s->bar, 0, sizeof(unsigned long long), s->stream));
+    CK(cudaMemsetAsync(s->rec_nnz, 0, sizeof(long long) * prm->max_iter, s->stream));
+    CK(cudaMemsetAsync(s->rec_dmax, 0, sizeof(unsigned long long) * prm->max_iter, s->stream));
     CK(cudaEventRecord(s->ev[1], s->stream));
 
     WformArgs a;
@@ -405,7 +428,19 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     a.rec_obj = s->rec_obj;
     a.rec_time = s->rec_time;
     a.rec_nnz = s->rec_nnz;
+    a.rec_dmax = s->rec_dmax;
+    a.share = s->share;
+    a.list_rs = s->list_rs;
+    a.list_dn = s->list_dn;
+    a.list_cnt = s->list_cnt;
     a.status = s->status;
+    unsigned long long* prof = nullptr;
+    const bool want_prof = getenv("CONCORD_PHASE_PROFILE") != nullptr;
+    if (want_prof) {
+        CK(dalloc(&prof, 16));
+        CK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), s->stream));
+    }
+    a.prof = prof;
     CK(launch_pcd_wform(a, s->nblk, s->stream));
     CK(cudaEventRecord(s->ev[2], s->stream));
     CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk, s->edges, s->stream));
@@ -441,6 +476,22 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
             }
         } else {
             for (int i = 0; i < iters; ++i) objective_trace[i] = NAN;
+        }
+    }
+    if (want_prof) {
+        unsigned long long pc[16];
+        CK(cudaMemcpy(pc, prof, sizeof(pc), cudaMemcpyDeviceToHost));
+        cudaFree(prof);
+        int clk_khz = 0;
+        cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, s->dev);
+        const double colours = (double)iters * (a.m);
+        const char* names[9] = {"wait", "publish", "share+arrive", "apply", "prefetch", "diag dense pass",
+                                "records", "-", "-"};
+        fprintf(stderr, "[concord phase profile] p=%d iters=%d clk=%d kHz (CTA 0)\n", s->p, iters, clk_khz);
+        for (int i = 0; i < 7; ++i) {
+            const double us = pc[i] / (clk_khz * 1e-3);
+            fprintf(stderr, "  %-20s %12.1f us total  %9.3f us/%s\n", names[i], us,
+                    i < 5 ? us / (colours + iters) : us / iters, i < 5 ? "phase" : "sweep");
         }
     }
     float setup_ms = 0.f, kernel_ms = 0.f;

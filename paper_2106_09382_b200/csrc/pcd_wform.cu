@@ -32,85 +32,234 @@ namespace concord {
 
 constexpr int kThreads = WFORM_THREADS;
 constexpr int kCap = WFORM_LIST_CAP;  // list entries (pairs) / diag rows per chunk
+constexpr int kUnroll = 2;            // independent row-stream items per thread in flight
+constexpr int kMaxBlocks = WFORM_MAX_BLOCKS;
 
+// Pair q of round k without integer division: c1 = m - 1 - k (common.cuh has the closed form).
+__device__ __forceinline__ void round_pair(int q, int m, int c1, int& r, int& s) {
+    int a, b;
+    if (q == 0) {
+        a = 0;
+        b = 1 + c1;
+    } else {
+        const int t = q + c1;
+        const int u = m + c1 - q;
+        a = 1 + (t >= m ? t - m : t);
+        b = 1 + (u >= m ? u - m : u);
+    }
+    r = min(a, b);
+    s = max(a, b);
+}
+
+// delta of pair (r, s) from the published half values vr = (W[s,r], Om[s,r]),
+// vs = (W[r,s], Om[r,s]); same operation order as offdiag_from_sums, with the
+// division skipped when the soft threshold returns its exact 0.0.
+__device__ __forceinline__ double pair_delta(double2 vr, double2 vs, double trr, double tss, double shrink,
+                                             double& nv) {
+    const double om = vs.y;
+    const double num = -__dsub_rn(__dadd_rn(vs.x, vr.x), __dmul_rn(om, __dadd_rn(tss, trr)));
+    const double av = __dsub_rn(fabs(num), shrink);
+    nv = (av <= 0.0) ? 0.0 : __ddiv_rn(num > 0.0 ? av : -av, __dadd_rn(trr, tss));
+    return __dsub_rn(nv, om);
+}
+
+__device__ __forceinline__ double diag_delta(double2 v, double tii, double n) {
+    return __dsub_rn(diag_from_dot(v.x, v.y, tii, n), v.y);
+}
+
+// Row published for column c in phase ph (ph < m: colour ph, ph == m: diagonal), or -1.
+__device__ __forceinline__ int pub_row(int ph, int c, int m, int p) {
+    const int x = (ph < m) ? circle_partner(c, ph, m) : c;
+    return x < p ? x : -1;
+}
+
+// Row whose value moves row x in phase ph (its pair partner; x itself on the diagonal).
+__device__ __forceinline__ int src_row(int ph, int x, int m) { return ph < m ? circle_partner(x, ph, m) : x; }
+
+// Phase-ph delta of row x (paired with y) recomputed from that phase's publish buffer.
+__device__ __forceinline__ double row_delta(int ph, int x, int y, const double2* pb, const double* tdiag, int m,
+                                            double shrink, double n, double& nv) {
+    if (ph < m) {
+        const int r = min(x, y), s = max(x, y);
+        return pair_delta(ldcg2(pb + r), ldcg2(pb + s), __ldg(tdiag + r), __ldg(tdiag + s), shrink, nv);
+    }
+    const double2 v = ldcg2(pb + x);
+    nv = diag_from_dot(v.x, v.y, __ldg(tdiag + x), n);
+    return __dsub_rn(nv, v.y);
+}
+
+__device__ __forceinline__ void bar_arrive(unsigned long long* ctr) {
+    // caller has done __syncthreads(); the fence makes the CTA's writes visible first
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1ull);
+    }
+}
+
+__device__ __forceinline__ void bar_wait(const unsigned long long* ctr, unsigned long long target) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire_u64(ctr) < target) {
+        }
+    }
+    __syncthreads();
+}
+
+// One grid barrier per phase (phase = one colour, or the diagonal step), with
+// the work split so that only a few hundred cycles sit between a barrier
+// release and the next arrive:
+//
+//   wait(G)       publishes of phase G (and the delta lists of phase G-1) are visible
+//   publish G+1   each column owner publishes (W[x,c], Om[x,c]) of its next cell;
+//                 the value was prefetched two phases ago and is brought forward
+//                 with the phase G-1 and phase G deltas of row x (recomputed from
+//                 the publish buffers: two closed forms and two FMAs, bitwise the
+//                 values the bulk row streams produce)
+//   share G       the CTA evaluates ITS 1/nblk of the colour's closed forms and
+//                 writes the non-zero (r, s, delta, new) to its list segment
+//   arrive(G+1)
+//   apply G-1     stream the previous phase's non-zero rows into the own slab --
+//                 after the arrive, i.e. overlapped with the barrier
+//   prefetch      the cell the next publish needs
+//
+// Publish buffers and delta lists rotate over 3 slots (phase mod 3): a CTA
+// still applying phase G-1 must not see it overwritten by a CTA already in G+1.
 __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int2* L_rs = reinterpret_cast<int2*>(smem_raw);
     double* L_d = reinterpret_cast<double*>(smem_raw + kCap * sizeof(int2));
-    double* D_d = reinterpret_cast<double*>(smem_raw);             // diag chunk: delta
-    double* D_new = reinterpret_cast<double*>(smem_raw) + kCap;    // diag chunk: new value
-    int* pubrow = reinterpret_cast<int*>(smem_raw + kCap * 16);
+    double* D_d = reinterpret_cast<double*>(smem_raw);           // diag chunk: delta
+    double* D_new = reinterpret_cast<double*>(smem_raw) + kCap;  // diag chunk: new value
+    __shared__ int s_off[kMaxBlocks + 1];
     __shared__ int s_cnt;
-    __shared__ double s_red[5][kThreads / 32];
+    __shared__ double s_red[5][32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.x;
-    const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1;
+    const int b = blockIdx.x, nblk = gridDim.x;
+    const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half;
     const int c0 = b * w;
     const int wl = min(w, p - c0);
+    const int c = c0 + tid;  // own column of a publisher thread (tid < wl)
+    const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
     double* __restrict__ Wb = a.W + (long long)b * a.slab;
     const double* __restrict__ Tb = a.T + (long long)b * a.slab;
     double* __restrict__ Ob = a.Om + (long long)b * a.slab;
-    const unsigned long long nb = gridDim.x;
+    const unsigned long long nbu = (unsigned long long)nblk;
     unsigned long long epoch = 0;
-    unsigned g = 0;  // phase counter, selects the ping-pong publish buffer
 
-    // Publish colour 0 of the first sweep.
+    // ---- publish phase 0 of the first sweep, arrive
     if (tid < wl) {
-        const int c = c0 + tid;
-        const int x = circle_partner(c, 0, m);
-        if (x < p) a.pub[c] = make_double2(Wb[(long long)x * w + tid], Ob[(long long)x * w + tid]);
+        const int x = pub_row(0, c, m, p);
+        if (x >= 0) a.pub[c] = make_double2(Wb[(long long)x * w + tid], Ob[(long long)x * w + tid]);
     }
+    __syncthreads();
+    bar_arrive(a.bar);
     if (b == 0 && tid == 0) a.rec_time[0] = globaltimer_ns();
 
-    int it = 0, converged = 0;
-    double dmax_blk = 0.0;
-    while (it < a.max_iter) {
-        double dmax = 0.0;
-        int nnz = 0;  // non-zero pair deltas seen by this thread in this sweep
-        // ------------------------------------------------------ colour steps
-        for (int k = 0; k < m; ++k) {
-            // Next phase's publish cell for each own column; prefetch it so the
-            // load overlaps the barrier wait.  Rows updated in this colour are
-            // re-captured by the apply loop below.
-            int xn = -1;
-            double2 pre = make_double2(0.0, 0.0);
-            if (tid < wl) {
-                const int c = c0 + tid;
-                xn = (k + 1 < m) ? circle_partner(c, k + 1, m) : c;
-                if (xn < p) {
-                    pre = make_double2(Wb[(long long)xn * w + tid], Ob[(long long)xn * w + tid]);
-                } else {
-                    xn = -1;
-                }
+    // ---- publisher state: cell (xp, c) for the next publish, prefetched value `pre`
+    // (W after every phase before ph0), brought forward by phases ph0 (source row y0,
+    // T[y0,c] = t0) and ph1 (y1, t1) at publish time.
+    int xp = -1, ph0 = -1, y0 = -1, ph1 = 0, y1 = -1;
+    double2 pre = make_double2(0.0, 0.0);
+    double t0 = 0.0, t1 = 0.0;
+    // prefetch for the publish done in phase `phA` (which publishes phase phA+1);
+    // `phB` is the phase before phA, or -1 when nothing precedes it.
+    auto prefetch = [&](int phB, int phA) {
+        xp = -1;
+        if (tid < wl) {
+            const int phn = (phA == m) ? 0 : phA + 1;
+            const int x = pub_row(phn, c, m, p);
+            if (x >= 0) {
+                xp = x;
+                ph0 = phB;
+                ph1 = phA;
+                y0 = (phB >= 0) ? src_row(phB, x, m) : p;
+                y1 = src_row(phA, x, m);
+                pre = make_double2(Wb[(long long)x * w + tid], Ob[(long long)x * w + tid]);
+                t0 = (y0 < p) ? __ldg(Tb + (long long)y0 * w + tid) : 0.0;
+                t1 = (y1 < p) ? __ldg(Tb + (long long)y1 * w + tid) : 0.0;
             }
-            if (tid < w) pubrow[tid] = xn;
-            grid_barrier(a.bar, (++epoch) * nb);
-            const double2* __restrict__ pb = a.pub + (size_t)(g & 1) * p;
-            double2* __restrict__ pn = a.pub + (size_t)((g + 1) & 1) * p;
+        }
+    };
+    prefetch(-1, 0);
 
-            for (int q0 = 0; q0 < a.half; q0 += kCap) {
+    // optional phase profile (CONCORD_PHASE_PROFILE): CTA 0 / thread 0 clock64 per phase
+    unsigned long long* prof = (a.prof && b == 0 && tid == 0) ? a.prof : nullptr;
+    long long tmark = clock64();
+#define PMARK(i)                                     \
+    if (prof) {                                      \
+        const long long t_ = clock64();              \
+        prof[i] += (unsigned long long)(t_ - tmark); \
+        tmark = t_;                                  \
+    }
+
+    int slot = 0;  // slot of the current phase; (slot+2)%3 is the previous one
+    int it = 0, converged = 0;
+    double smax = 0.0;  // max |delta| over this thread's share of the sweep
+    int snnz = 0;
+    while (true) {
+        for (int ph = 0; ph <= m; ++ph) {
+            bar_wait(a.bar, (++epoch) * nbu);
+            PMARK(0);
+            const int pslot = (slot == 0) ? 2 : slot - 1;
+            const int nslot = (slot == 2) ? 0 : slot + 1;
+            const double2* __restrict__ pb = a.pub + (size_t)slot * p;
+            const double2* __restrict__ pbm = a.pub + (size_t)pslot * p;
+            double2* __restrict__ pn = a.pub + (size_t)nslot * p;
+            const bool diag = (ph == m);
+
+            // ---- diagonal: convergence decision first (every CTA sees the same values)
+            bool stop = false;
+            double dmax_all = 0.0;
+            if (diag) {
+                double dm = 0.0;
+                for (int i = tid; i < p; i += kThreads)
+                    dm = fmax(dm, fabs(diag_delta(ldcg2(pb + i), __ldg(a.tdiag + i), a.n)));
+                dm = warp_max(dm);
+                if (lane == 0) s_red[0][warp] = dm;
+                __syncthreads();
+                const double off = __longlong_as_double((long long)__ldcg(a.rec_dmax + it));
+                dmax_all = fmax(off, warp_max(lane < kThreads / 32 ? s_red[0][lane] : 0.0));
+                stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter);
+                __syncthreads();
+            }
+
+            // ---- publish phase ph+1
+            if (!stop && xp >= 0) {
+                double val = pre.x, om = pre.y, nv;
+                if (y0 < p) {
+                    const double d = row_delta(ph0, xp, y0, pbm, a.tdiag, m, a.shrink, a.n, nv);
+                    if (d != 0.0) val = fma(d, t0, val);
+                    if (y0 == c) om = nv;  // the correcting phase moved this very cell (only when m == 1)
+                }
+                if (y1 < p) {
+                    const double d = row_delta(ph1, xp, y1, pb, a.tdiag, m, a.shrink, a.n, nv);
+                    if (d != 0.0) val = fma(d, t1, val);
+                    if (y1 == c) om = nv;
+                }
+                pn[c] = make_double2(val, om);
+            }
+            PMARK(1);
+
+            // ---- share of the colour's closed forms -> list segment of this CTA
+            if (!diag) {
                 if (tid == 0) s_cnt = 0;
                 __syncthreads();
-                const int qend = min(q0 + kCap, a.half);
-                for (int base = q0; base < qend; base += kThreads) {
-                    const int q = base + tid;
+                const int c1 = m - 1 - ph;
+                int2* seg_rs = a.list_rs + ((size_t)slot * nblk + b) * a.share;
+                double2* seg_dn = a.list_dn + ((size_t)slot * nblk + b) * a.share;
+                const int sid = kThreads - 1 - tid;  // share work starts on the last warps
+                for (int base = q_lo; base < q_hi; base += kThreads) {
+                    const int q = base + sid;
                     int r = 0, s = 0;
-                    double d = 0.0;
-                    if (q < qend) {
-                        circle_pair(k, q, m, r, s);
+                    double d = 0.0, nv = 0.0;
+                    if (q < q_hi) {
+                        round_pair(q, m, c1, r, s);
                         if (s < p) {
-                            const double2 vr = ldcg2(pb + r);  // (W[s,r], Om[s,r])
-                            const double2 vs = ldcg2(pb + s);  // (W[r,s], Om[r,s])
-                            const double trr = __ldg(a.tdiag + r), tss = __ldg(a.tdiag + s);
-                            const double om = vs.y;
-                            const double nv = offdiag_from_sums(vs.x, vr.x, om, trr, tss, a.shrink);
-                            d = __dsub_rn(nv, om);
+                            d = pair_delta(ldcg2(pb + r), ldcg2(pb + s), __ldg(a.tdiag + r), __ldg(a.tdiag + s),
+                                           a.shrink, nv);
                             if (d != 0.0) {
-                                dmax = fmax(dmax, fabs(d));
-                                ++nnz;
-                                if ((unsigned)(s - c0) < (unsigned)wl) Ob[(long long)r * w + (s - c0)] = nv;
-                                if ((unsigned)(r - c0) < (unsigned)wl) Ob[(long long)s * w + (r - c0)] = nv;
+                                smax = fmax(smax, fabs(d));
+                                ++snnz;
                             }
                         }
                     }
@@ -120,153 +269,234 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         if (lane == 0) basepos = atomicAdd(&s_cnt, __popc(mask));
                         basepos = __shfl_sync(0xffffffffu, basepos, 0);
                         if (d != 0.0) {
-                            const int slot = basepos + __popc(mask & ((1u << lane) - 1u));
-                            L_rs[slot] = make_int2(r, s);
-                            L_d[slot] = d;
+                            const int at = basepos + __popc(mask & ((1u << lane) - 1u));
+                            seg_rs[at] = make_int2(r, s);
+                            seg_dn[at] = make_double2(d, nv);
                         }
                     }
                 }
-                if (q0 == 0 && xn >= 0) pn[c0 + tid] = pre;
                 __syncthreads();
-                const int cnt = s_cnt;
-                const int per = 2 * w2;
-                const int items = cnt * per;
-                for (int idx = tid; idx < items; idx += kThreads) {
-                    const int e = idx / per;
-                    const int rem = idx - e * per;
-                    const int h = rem >= w2;
-                    const int j2 = rem - h * w2;
-                    const int2 rs = L_rs[e];
-                    const double d = L_d[e];
-                    const int dst = h ? rs.y : rs.x;
-                    const int src = h ? rs.x : rs.y;
-                    double2* wp = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
-                    const double2 tv = __ldg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
-                    double2 wv = *wp;
-                    wv.x = fma(d, tv.x, wv.x);
-                    wv.y = fma(d, tv.y, wv.y);
-                    *wp = wv;
-                    const int j = 2 * j2;
-                    if (pubrow[j] == dst) pn[c0 + j].x = wv.x;
-                    if (pubrow[j + 1] == dst) pn[c0 + j + 1].x = wv.y;
-                }
-                __syncthreads();
-            }
-            ++g;
-        }
-
-        // ------------------------------------------------------ diagonal step
-        int x0 = -1;
-        double pre_om = 0.0;
-        if (tid < wl) {
-            const int c = c0 + tid;
-            x0 = circle_partner(c, 0, m);
-            if (x0 < p) pre_om = Ob[(long long)x0 * w + tid];
-            else x0 = -1;
-        }
-        grid_barrier(a.bar, (++epoch) * nb);
-        if (tid < w) pubrow[tid] = x0;
-        const double2* __restrict__ pb = a.pub + (size_t)(g & 1) * p;
-        double2* __restrict__ pn = a.pub + (size_t)((g + 1) & 1) * p;
-        if (x0 >= 0) pn[c0 + tid].y = pre_om;  // .x is captured by the dense pass
-        double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
-        for (int i0 = 0; i0 < p; i0 += kCap) {
-            const int iend = min(i0 + kCap, p);
-            __syncthreads();
-            for (int i = i0 + tid; i < iend; i += kThreads) {
-                const double2 v = ldcg2(pb + i);  // (W[i,i], Om[i,i])
-                const double tii = __ldg(a.tdiag + i);
-                const double nv = diag_from_dot(v.x, v.y, tii, a.n);
-                const double d = __dsub_rn(nv, v.y);
-                dmax = fmax(dmax, fabs(d));
-                D_d[i - i0] = d;
-                D_new[i - i0] = nv;
-            }
-            __syncthreads();
-            const int items = (iend - i0) * w2;
-            for (int idx = tid; idx < items; idx += kThreads) {
-                const int ii = idx / w2;
-                const int j2 = idx - ii * w2;
-                const int i = i0 + ii;
-                const double d = D_d[ii];
-                double2* wp = reinterpret_cast<double2*>(Wb + (long long)i * w) + j2;
-                double2 wv = *wp;
-                if (d != 0.0) {
-                    const double2 tv = __ldg(reinterpret_cast<const double2*>(Tb + (long long)i * w) + j2);
-                    wv.x = fma(d, tv.x, wv.x);
-                    wv.y = fma(d, tv.y, wv.y);
-                    *wp = wv;
-                }
-                const int j = 2 * j2;
-                const int cj = c0 + j;
-                if (pubrow[j] == i) pn[cj].x = wv.x;
-                if (pubrow[j + 1] == i) pn[cj + 1].x = wv.y;
-                const bool dg0 = (cj == i), dg1 = (cj + 1 == i);
-                if (a.want_trace) {
-                    double2* op = reinterpret_cast<double2*>(Ob + (long long)i * w) + j2;
-                    double2 ov = *op;
-                    if (dg0 | dg1) {
-                        if (dg0) ov.x = D_new[ii];
-                        if (dg1) ov.y = D_new[ii];
-                        *op = ov;
-                        log_acc += log(D_new[ii]);
+                if (tid == 0) a.list_cnt[(size_t)slot * nblk + b] = s_cnt;
+                if (ph == m - 1) {  // flush this sweep's share statistics
+                    const double mw = warp_max(smax);
+                    const double nw = warp_sum((double)snnz);
+                    if (lane == 0) {
+                        s_red[0][warp] = mw;
+                        s_red[1][warp] = nw;
                     }
-                    q_acc = fma(wv.x, ov.x, q_acc);
-                    q_acc = fma(wv.y, ov.y, q_acc);
-                    if (i < cj) pen_acc += fabs(ov.x);
-                    if (i < cj + 1) pen_acc += fabs(ov.y);
-                } else if (dg0 | dg1) {
-                    Ob[(long long)i * w + (dg0 ? j : j + 1)] = D_new[ii];
+                    __syncthreads();
+                    if (warp == 0) {
+                        const bool in = lane < kThreads / 32;
+                        const double mb = warp_max(in ? s_red[0][lane] : 0.0);
+                        const double nbk = warp_sum(in ? s_red[1][lane] : 0.0);
+                        if (lane == 0) {
+                            atomicMax(a.rec_dmax + it, (unsigned long long)__double_as_longlong(mb));
+                            atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + it),
+                                      (unsigned long long)nbk);
+                        }
+                    }
+                    smax = 0.0;
+                    snnz = 0;
                 }
             }
-        }
-        ++g;
-        ++it;
+            PMARK(2);
+            if (!stop) {
+                __syncthreads();
+                bar_arrive(a.bar);
+            }
 
-        // ------------------------------------------------- block reductions
-        dmax = warp_max(dmax);
-        q_acc = warp_sum(q_acc);
-        pen_acc = warp_sum(pen_acc);
-        log_acc = warp_sum(log_acc);
-        const double nnz_w = warp_sum((double)nnz);
-        if (lane == 0) {
-            s_red[0][warp] = dmax;
-            s_red[1][warp] = q_acc;
-            s_red[2][warp] = pen_acc;
-            s_red[3][warp] = log_acc;
-            s_red[4][warp] = nnz_w;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double v0 = s_red[0][lane], v1 = s_red[1][lane], v2 = s_red[2][lane], v3 = s_red[3][lane];
-            const double v4 = warp_sum(s_red[4][lane]);
-            v0 = warp_max(v0);
-            v1 = warp_sum(v1);
-            v2 = warp_sum(v2);
-            v3 = warp_sum(v3);
-            if (lane == 0) {
-                s_red[0][0] = v0;
-                if (a.want_trace) {
-                    double* ro = a.rec_obj + ((size_t)(it - 1) * gridDim.x + b) * 3;
-                    ro[0] = v1;
-                    ro[1] = v2;
-                    ro[2] = v3;
+            // ---- apply the previous colour's non-zero deltas to the own slab
+            const int prev = (ph == 0) ? -1 : ph - 1;  // phase 0 follows the diagonal (already applied)
+            if (prev >= 0 && (it > 0 || ph > 0)) {
+                for (int j = tid; j < nblk; j += kThreads) s_off[j] = __ldcg(a.list_cnt + (size_t)pslot * nblk + j);
+                __syncthreads();
+                if (warp == 0) {
+                    int run = 0;
+                    for (int j0 = 0; j0 < nblk; j0 += 32) {
+                        const int j = j0 + lane;
+                        int v = (j < nblk) ? s_off[j] : 0;
+                        int incl = v;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += t;
+                        }
+                        if (j < nblk) s_off[j] = run + incl - v;
+                        run += __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                    if (lane == 0) s_off[nblk] = run;
                 }
-                if (b == 0) {
-                    a.rec_delta[it - 1] = v0;
-                    a.rec_nnz[it - 1] = (long long)v4;
-                    a.rec_time[it] = globaltimer_ns();
+                __syncthreads();
+                const int total = s_off[nblk];
+                const int2* lrs = a.list_rs + (size_t)pslot * nblk * a.share;
+                const double2* ldn = a.list_dn + (size_t)pslot * nblk * a.share;
+                for (int e0 = 0; e0 < total; e0 += kCap) {
+                    const int e1 = min(total, e0 + kCap);
+                    for (int e = e0 + tid; e < e1; e += kThreads) {
+                        int lo = 0, hi = nblk;  // segment: s_off[lo] <= e < s_off[lo+1]
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (s_off[mid] <= e) lo = mid;
+                            else hi = mid;
+                        }
+                        const size_t at = (size_t)lo * a.share + (e - s_off[lo]);
+                        const int2 rs = __ldcg(lrs + at);
+                        const double2 dn = __ldcg(ldn + at);
+                        if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
+                        if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                        L_rs[e - e0] = rs;
+                        L_d[e - e0] = dn.x;
+                    }
+                    __syncthreads();
+                    const int per = 2 * w2;
+                    const int items = (e1 - e0) * per;
+                    for (int base = 0; base < items; base += kThreads * kUnroll) {
+                        double2 tv[kUnroll], wv[kUnroll];
+                        double2* wp[kUnroll];
+                        double dd[kUnroll];
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int idx = base + u * kThreads + tid;
+                            wp[u] = nullptr;
+                            if (idx < items) {
+                                const int e = idx / per;
+                                const int rem = idx - e * per;
+                                const int h = rem >= w2;
+                                const int j2 = rem - h * w2;
+                                const int2 rs = L_rs[e];
+                                dd[u] = L_d[e];
+                                const int dst = h ? rs.y : rs.x;
+                                const int src = h ? rs.x : rs.y;
+                                wp[u] = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
+                                tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
+                                wv[u] = *wp[u];
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            if (wp[u]) {
+                                wv[u].x = fma(dd[u], tv[u].x, wv[u].x);
+                                wv[u].y = fma(dd[u], tv[u].y, wv[u].y);
+                                *wp[u] = wv[u];
+                            }
+                        }
+                    }
+                    __syncthreads();
                 }
             }
+            PMARK(3);
+
+            if (!diag) {
+                prefetch(ph, ph + 1);
+                PMARK(4);
+                slot = nslot;
+                continue;
+            }
+
+            // ---- diagonal step: prefetch (W before this phase), then the dense slab stream
+            if (!stop) prefetch(m, 0);
+            double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
+            for (int i0 = 0; i0 < p; i0 += kCap) {
+                const int iend = min(i0 + kCap, p);
+                for (int i = i0 + tid; i < iend; i += kThreads) {
+                    const double2 v = ldcg2(pb + i);
+                    const double nv = diag_from_dot(v.x, v.y, __ldg(a.tdiag + i), a.n);
+                    D_d[i - i0] = __dsub_rn(nv, v.y);
+                    D_new[i - i0] = nv;
+                }
+                __syncthreads();
+                const int items = (iend - i0) * w2;
+                for (int base = 0; base < items; base += kThreads * kUnroll) {
+                    double2 wv[kUnroll], tv[kUnroll], ov[kUnroll];
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        const int idx = base + u * kThreads + tid;
+                        if (idx < items) {
+                            const int ii = idx / w2;
+                            const int j2 = idx - ii * w2;
+                            const long long off = (long long)(i0 + ii) * w + 2 * j2;
+                            wv[u] = *reinterpret_cast<const double2*>(Wb + off);
+                            if (D_d[ii] != 0.0) tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + off));
+                            if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        const int idx = base + u * kThreads + tid;
+                        if (idx < items) {
+                            const int ii = idx / w2;
+                            const int j2 = idx - ii * w2;
+                            const int i = i0 + ii;
+                            const long long off = (long long)i * w + 2 * j2;
+                            const double d = D_d[ii];
+                            if (d != 0.0) {
+                                wv[u].x = fma(d, tv[u].x, wv[u].x);
+                                wv[u].y = fma(d, tv[u].y, wv[u].y);
+                                *reinterpret_cast<double2*>(Wb + off) = wv[u];
+                            }
+                            const int cj = c0 + 2 * j2;
+                            const bool dg0 = (cj == i), dg1 = (cj + 1 == i);
+                            if (a.want_trace) {
+                                if (dg0 | dg1) {
+                                    if (dg0) ov[u].x = D_new[ii];
+                                    if (dg1) ov[u].y = D_new[ii];
+                                    *reinterpret_cast<double2*>(Ob + off) = ov[u];
+                                    log_acc += log(D_new[ii]);
+                                }
+                                q_acc = fma(wv[u].x, ov[u].x, q_acc);
+                                q_acc = fma(wv[u].y, ov[u].y, q_acc);
+                                if (i < cj) pen_acc += fabs(ov[u].x);
+                                if (i < cj + 1) pen_acc += fabs(ov[u].y);
+                            } else if (dg0 | dg1) {
+                                Ob[off + (dg0 ? 0 : 1)] = D_new[ii];
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            ++it;
+            PMARK(5);
+
+            // ---- per-sweep records
+            q_acc = warp_sum(q_acc);
+            pen_acc = warp_sum(pen_acc);
+            log_acc = warp_sum(log_acc);
+            if (lane == 0) {
+                s_red[1][warp] = q_acc;
+                s_red[2][warp] = pen_acc;
+                s_red[3][warp] = log_acc;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const bool in = lane < kThreads / 32;
+                const double v1 = warp_sum(in ? s_red[1][lane] : 0.0);
+                const double v2 = warp_sum(in ? s_red[2][lane] : 0.0);
+                const double v3 = warp_sum(in ? s_red[3][lane] : 0.0);
+                if (lane == 0) {
+                    if (a.want_trace) {
+                        double* ro = a.rec_obj + ((size_t)(it - 1) * nblk + b) * 3;
+                        ro[0] = v1;
+                        ro[1] = v2;
+                        ro[2] = v3;
+                    }
+                    if (b == 0) {
+                        a.rec_delta[it - 1] = dmax_all;
+                        a.rec_time[it] = globaltimer_ns();
+                    }
+                }
+            }
+            __syncthreads();
+            PMARK(6);
+            if (stop) {
+                converged = dmax_all < a.delta_tol;
+                break;
+            }
+            slot = nslot;
         }
-        __syncthreads();
-        dmax_blk = s_red[0][0];
-        __syncthreads();
-        if (dmax_blk < a.delta_tol) {
-            converged = 1;
-            break;
-        }
+        if (it > 0 && (converged || it >= a.max_iter)) break;
     }
+#undef PMARK
     if (b == 0 && tid == 0) {
         a.status[0] = it;
         a.status[1] = converged;

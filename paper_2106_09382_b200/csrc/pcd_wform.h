@@ -3,8 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#define WFORM_THREADS 1024
+#define WFORM_THREADS 512
 #define WFORM_LIST_CAP 4096
+#define WFORM_MAX_BLOCKS 1024
 
 namespace concord {
 
@@ -18,7 +19,7 @@ struct WformArgs {
     const double* T;
     double* Om;     // slab-major dense Omega
     const double* tdiag;
-    double2* pub;   // 2 * p ping-pong publish buffers
+    double2* pub;   // 3 * p rotating publish buffers (phase mod 3)
     double n;       // sample count (GramMatrix.n)
     double shrink;  // n * lam (solver.py:285)
     double delta_tol;
@@ -28,11 +29,17 @@ struct WformArgs {
     double* rec_delta;              // [max_iter]
     double* rec_obj;                // [max_iter][nblk][3]: <W,Om> part, sum_{i<j}|om|, sum log om_ii
     unsigned long long* rec_time;   // [max_iter + 1] globaltimer ns
-    long long* rec_nnz;             // [max_iter] non-zero off-diagonal deltas per sweep
+    long long* rec_nnz;             // [max_iter] non-zero off-diagonal deltas per sweep (zeroed by host)
+    unsigned long long* rec_dmax;   // [max_iter] max |off-diagonal delta| per sweep, double bits (zeroed)
+    int share;                      // pairs per CTA per colour = ceil(half / nblk)
+    int2* list_rs;                  // [3][nblk][share] non-zero pairs of a colour, per CTA segment
+    double2* list_dn;               // [3][nblk][share] (delta, new value)
+    int* list_cnt;                  // [3][nblk] segment lengths
     int* status;                    // [0] iterations, [1] converged
+    unsigned long long* prof;       // optional [16] phase cycle counters (CTA 0), or NULL
 };
 
-inline size_t wform_smem_bytes(int w) { return (size_t)WFORM_LIST_CAP * 16 + (size_t)w * sizeof(int); }
+inline size_t wform_smem_bytes(int w) { return (size_t)WFORM_LIST_CAP * 16 + 0 * (size_t)w; }
 
 cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st);
 cudaError_t wform_max_blocks(int w, int* max_blocks);
