@@ -90,6 +90,12 @@ struct concord_solver {
     unsigned long long* rec_dmax = nullptr;
     int rec_cap = 0;
     int share = 0;
+    int nsh = 0;
+    int lmax = 1;
+    int rd = 0;
+    int rl = 0;
+    double* dring = nullptr;
+    double2* diagd = nullptr;
     int2* list_rs = nullptr;
     double2* list_dn = nullptr;
     int* list_cnt = nullptr;
@@ -256,7 +262,7 @@ int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_s
     int max_blocks = 0;
     for (;;) {
         if (w > WFORM_THREADS) return fail(CONCORD_ERR_ARG, "p=%d needs slab width %d > %d", ip, w, WFORM_THREADS);
-        CK(wform_max_blocks(w, &max_blocks));
+        CK(wform_max_blocks(w, ip, &max_blocks));
         if ((ip + w - 1) / w <= max_blocks && (ip + w - 1) / w <= WFORM_MAX_BLOCKS) break;
         w += 2;
     }
@@ -290,11 +296,20 @@ int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_s
     CKC(dalloc(&s->pub, 3 * (size_t)ip));
     {
         const int half = (ip + (ip & 1)) / 2;
+        int share_min = WFORM_SHARE_MIN;
+        if (const char* e = getenv("CONCORD_SHARE_MIN")) share_min = atoi(e);
         s->share = (half + s->nblk - 1) / s->nblk;
-        const size_t entries = 3 * (size_t)s->nblk * s->share;
+        if (s->share < share_min) s->share = share_min < half ? share_min : half;
+        s->nsh = (half + s->share - 1) / s->share;
+        s->lmax = wform_lag_cap(w, 2 * half - 1);
+        s->rd = s->lmax + 3;
+        s->rl = s->lmax + 4;
+        const size_t entries = (size_t)s->rl * s->nblk * s->share;
         CKC(dalloc(&s->list_rs, entries));
         CKC(dalloc(&s->list_dn, entries));
-        CKC(dalloc(&s->list_cnt, 3 * (size_t)s->nblk));
+        CKC(dalloc(&s->list_cnt, (size_t)s->rl * s->nblk));
+        CKC(dalloc(&s->dring, (size_t)s->rd * ip));
+        CKC(dalloc(&s->diagd, (size_t)s->nblk * ip));
     }
     CKC(dalloc(&s->bar, 1));
     CKC(dalloc(&s->edges, 1));
@@ -327,6 +342,8 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->list_rs);
     cudaFree(s->list_dn);
     cudaFree(s->list_cnt);
+    cudaFree(s->dring);
+    cudaFree(s->diagd);
     cudaFree(s->csr_rowptr);
     cudaFree(s->csr_col);
     cudaFree(s->csr_val);
@@ -430,9 +447,19 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     a.rec_nnz = s->rec_nnz;
     a.rec_dmax = s->rec_dmax;
     a.share = s->share;
+    a.nsh = s->nsh;
+    a.stage_ahead = 3;
+    if (const char* e = getenv("CONCORD_STAGE_AHEAD")) a.stage_ahead = atoi(e);
+    if (a.stage_ahead < 2) a.stage_ahead = 2;
+    if (a.stage_ahead > 3) a.stage_ahead = 3;
     a.list_rs = s->list_rs;
     a.list_dn = s->list_dn;
     a.list_cnt = s->list_cnt;
+    a.dring = s->dring;
+    a.diagd = s->diagd;
+    a.lmax = s->lmax;
+    a.rd = s->rd;
+    a.rl = s->rl;
     a.status = s->status;
     unsigned long long* prof = nullptr;
     const bool want_prof = getenv("CONCORD_PHASE_PROFILE") != nullptr;
@@ -484,15 +511,19 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         cudaFree(prof);
         int clk_khz = 0;
         cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, s->dev);
-        const double colours = (double)iters * (a.m);
-        const char* names[9] = {"wait", "publish", "share+arrive", "apply", "prefetch", "diag dense pass",
-                                "records", "-", "-"};
-        fprintf(stderr, "[concord phase profile] p=%d iters=%d clk=%d kHz (CTA 0)\n", s->p, iters, clk_khz);
-        for (int i = 0; i < 7; ++i) {
+        const double phases = (double)pc[3];
+        fprintf(stderr, "[concord phase profile] p=%d iters=%d phases=%.0f lmax=%d clk=%d kHz (CTA 0)\n", s->p, iters,
+                phases, s->lmax, clk_khz);
+        const char* names[12] = {"chain: barrier wait", "chain: stage wait", "chain: publish+share+arrive", "-",
+                                 "apply: busy", "apply: idle", "apply: batches", "chain:  publish (tc0)",
+                                 "chain:  bar+fence+arrive", "chain:  share (last thread)", "apply:  heads+stage",
+                                 "apply:  diagonal steps"};
+        for (int i = 0; i < 12; ++i) {
+            if (i == 3 || i == 6) continue;
             const double us = pc[i] / (clk_khz * 1e-3);
-            fprintf(stderr, "  %-20s %12.1f us total  %9.3f us/%s\n", names[i], us,
-                    i < 5 ? us / (colours + iters) : us / iters, i < 5 ? "phase" : "sweep");
+            fprintf(stderr, "  %-30s %12.1f us total  %9.3f us/phase\n", names[i], us, us / (phases > 0 ? phases : 1));
         }
+        fprintf(stderr, "  %-30s %12llu (%.2f phases/batch)\n", names[6], pc[6], pc[6] ? phases / pc[6] : 0.0);
     }
     float setup_ms = 0.f, kernel_ms = 0.f;
     CK(cudaEventElapsedTime(&setup_ms, s->ev[0], s->ev[1]));

@@ -11,16 +11,34 @@
 // make most d exactly 0, and those rows are skipped exactly.
 //
 // Layout in HBM: T, W and dense Omega are column-block ("slab") major.  CTA b
-// owns columns [b*w, b*w+w); slab b is a p x w row-major block.  A pair's row
-// update only touches a CTA's own columns, so each colour needs ONE grid
-// barrier: owners publish (W[partner(c), c], Omega[partner(c), c]) for their
-// columns c into a ping-pong buffer, barrier, then every CTA recomputes all
-// p/2 closed forms of the colour redundantly (identical arithmetic, so
-// identical results in every CTA) and applies the non-zero ones to its slab.
-// The max |delta| convergence metric (solver.py:287) is therefore identical in
-// every CTA and the stop test needs no extra reduction.  The diagonal phase
-// (_ckernels.pyx:96-102) is one dense slab stream that also folds in the
-// objective trace (model.py:210-217) as 1/2 <W, Omega>.
+// owns columns [b*w, b*w+w); slab b is a p x w row-major block, so every row
+// stream only touches the CTA's own slab.
+//
+// Phases.  A sweep is m = p_even-1 colour phases then the diagonal phase
+// (_ckernels.pyx:81-102); phases are numbered globally, g = sweep*(m+1) + ph.
+// Each CTA runs two warp-specialised roles:
+//
+//  * chain warps (WFORM_CHAIN_WARPS): the latency-critical colour chain.  Per
+//    phase g: wait on the grid barrier (all publishes of g visible); publish
+//    (W[x,c], Om[x,c]) of every own column c for phase g+1 (x = partner of c);
+//    evaluate this CTA's 1/nblk share of the colour-g closed forms
+//    (_ckernels.pyx:25-38) and write the per-row deltas (dring) and the
+//    non-zero (r, s, delta, new) list; arrive.  One grid barrier per phase.
+//  * apply warps (the rest): stream the delta lists into the own slab -- in
+//    phase order, batched over up to WFORM_BATCH phases, trailing the chain by
+//    up to `lmax` phases -- and the dense diagonal step (also folding in the
+//    objective trace, model.py:210-217).  After each batch they stage, in
+//    shared memory, the W/Om cells the next publishes need together with the
+//    T entries of the phases they have not applied yet.
+//
+// A publish therefore starts from a staged value W[x,c] that includes every
+// phase <= C (the apply watermark) and brings it forward with
+//   W[x,c] = fma(d_k, T[src_k(x), c], W[x,c])   for k = C+1 .. g, d_k != 0
+// -- the very operations, in the very order, the apply warps perform on the
+// slab -- so every published value is bitwise the value of the sequential
+// W-form.  d_k comes from dring for k < g and is recomputed from the phase-g
+// publish buffer for k = g.  Every CTA sees identical values, so the max
+// |delta| convergence metric (solver.py:287) needs no extra reduction.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -31,9 +49,15 @@
 namespace concord {
 
 constexpr int kThreads = WFORM_THREADS;
-constexpr int kCap = WFORM_LIST_CAP;  // list entries (pairs) / diag rows per chunk
-constexpr int kUnroll = 2;            // independent row-stream items per thread in flight
-constexpr int kMaxBlocks = WFORM_MAX_BLOCKS;
+constexpr int kChainWarps = WFORM_CHAIN_WARPS;
+constexpr int kChain = kChainWarps * 32;
+constexpr int kApply = kThreads - kChain;
+constexpr int kApplyWarps = kApply / 32;
+constexpr int kPairCap = WFORM_PAIR_CAP;
+constexpr int kBatch = WFORM_BATCH;
+constexpr int kSlots = WFORM_STAGE_SLOTS;
+constexpr int kMaxLag = WFORM_MAX_LAG;
+constexpr int kUnroll = 2;
 
 // Pair q of round k without integer division: c1 = m - 1 - k (common.cuh has the closed form).
 __device__ __forceinline__ void round_pair(int q, int m, int c1, int& r, int& s) {
@@ -63,10 +87,6 @@ __device__ __forceinline__ double pair_delta(double2 vr, double2 vs, double trr,
     return __dsub_rn(nv, om);
 }
 
-__device__ __forceinline__ double diag_delta(double2 v, double tii, double n) {
-    return __dsub_rn(diag_from_dot(v.x, v.y, tii, n), v.y);
-}
-
 // Row published for column c in phase ph (ph < m: colour ph, ph == m: diagonal), or -1.
 __device__ __forceinline__ int pub_row(int ph, int c, int m, int p) {
     const int x = (ph < m) ? circle_partner(c, ph, m) : c;
@@ -78,7 +98,8 @@ __device__ __forceinline__ int src_row(int ph, int x, int m) { return ph < m ? c
 
 // Phase-ph delta of row x (paired with y) recomputed from that phase's publish buffer.
 __device__ __forceinline__ double row_delta(int ph, int x, int y, const double2* pb, const double* tdiag, int m,
-                                            double shrink, double n, double& nv) {
+                                            double shrink, double n) {
+    double nv;
     if (ph < m) {
         const int r = min(x, y), s = max(x, y);
         return pair_delta(ldcg2(pb + r), ldcg2(pb + s), __ldg(tdiag + r), __ldg(tdiag + s), shrink, nv);
@@ -88,167 +109,286 @@ __device__ __forceinline__ double row_delta(int ph, int x, int y, const double2*
     return __dsub_rn(nv, v.y);
 }
 
-__device__ __forceinline__ void bar_arrive(unsigned long long* ctr) {
-    // caller has done __syncthreads(); the fence makes the CTA's writes visible first
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1ull);
+__device__ __forceinline__ void bar_chain() { asm volatile("bar.sync 1, %0;" ::"n"(kChain) : "memory"); }
+__device__ __forceinline__ void bar_apply() { asm volatile("bar.sync 2, %0;" ::"n"(kApply) : "memory"); }
+
+__device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
+// Exclusive scan of s[0..n) in place by the apply warps; returns the total (also in s[n]).
+__device__ int apply_scan(int* s, int n, int ta, int* s_wsum) {
+    const int lane = ta & 31, wa = ta >> 5;
+    const int per = (n + kApply - 1) / kApply;
+    const int lo = min(n, ta * per), hi = min(n, lo + per);
+    int local = 0;
+    for (int i = lo; i < hi; ++i) local += s[i];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
     }
+    if (lane == 31) s_wsum[wa] = incl;
+    bar_apply();
+    int wbase = 0, total = 0;
+    for (int j = 0; j < kApplyWarps; ++j) {
+        const int v = s_wsum[j];
+        if (j < wa) wbase += v;
+        total += v;
+    }
+    int run = wbase + incl - local;
+    for (int i = lo; i < hi; ++i) {
+        const int v = s[i];
+        s[i] = run;
+        run += v;
+    }
+    if (ta == 0) s[n] = total;
+    bar_apply();
+    return total;
 }
 
-__device__ __forceinline__ void bar_wait(const unsigned long long* ctr, unsigned long long target) {
-    if (threadIdx.x == 0) {
-        while (ld_acquire_u64(ctr) < target) {
+// Row streams of delta-list entries [e_lo, e_hi) (shared-memory indices; only
+// batch phase `only` when only >= 0): W[dst, own] = fma(d, T[src, own], W[dst, own])
+// for both rows of every pair.
+__device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, const int* L_ph, int only, int e_lo,
+                                           int e_hi, int w2, double* __restrict__ Wb, const double* __restrict__ Tb,
+                                           int ta) {
+    const int w = 2 * w2;
+    const int per = 2 * w2;
+    const int items = (e_hi - e_lo) * per;
+    for (int base = 0; base < items; base += kApply * kUnroll) {
+        double2 tv[kUnroll], wv[kUnroll];
+        double2* wp[kUnroll];
+        double dd[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int idx = base + u * kApply + ta;
+            wp[u] = nullptr;
+            if (idx < items) {
+                const int e = e_lo + idx / per;
+                if (only < 0 || L_ph[e] == only) {
+                    const int rem = idx - (idx / per) * per;
+                    const int h = rem >= w2;
+                    const int j2 = rem - h * w2;
+                    const int2 rs = L_rs[e];
+                    dd[u] = L_d[e];
+                    const int dst = h ? rs.y : rs.x;
+                    const int src = h ? rs.x : rs.y;
+                    wp[u] = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
+                    tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
+                    wv[u] = *wp[u];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (wp[u]) {
+                wv[u].x = fma(dd[u], tv[u].x, wv[u].x);
+                wv[u].y = fma(dd[u], tv[u].y, wv[u].y);
+                *wp[u] = wv[u];
+            }
         }
     }
-    __syncthreads();
 }
 
-// One grid barrier per phase (phase = one colour, or the diagonal step), with
-// the work split so that only a few hundred cycles sit between a barrier
-// release and the next arrive:
-//
-//   wait(G)       publishes of phase G (and the delta lists of phase G-1) are visible
-//   publish G+1   each column owner publishes (W[x,c], Om[x,c]) of its next cell;
-//                 the value was prefetched two phases ago and is brought forward
-//                 with the phase G-1 and phase G deltas of row x (recomputed from
-//                 the publish buffers: two closed forms and two FMAs, bitwise the
-//                 values the bulk row streams produce)
-//   share G       the CTA evaluates ITS 1/nblk of the colour's closed forms and
-//                 writes the non-zero (r, s, delta, new) to its list segment
-//   arrive(G+1)
-//   apply G-1     stream the previous phase's non-zero rows into the own slab --
-//                 after the arrive, i.e. overlapped with the barrier
-//   prefetch      the cell the next publish needs
-//
-// Publish buffers and delta lists rotate over 3 slots (phase mod 3): a CTA
-// still applying phase G-1 must not see it overwritten by a CTA already in G+1.
+struct Smem {
+    double* stage;  // [kSlots][2 + lmax][w]: W, Om, T of the uncovered phases
+    int* s_off;     // [kBatch * nblk + 1]
+    int2* L_rs;     // [kPairCap]
+    double* L_d;    // [kPairCap]  (diag chunk: delta)
+    double* L_new;  // [kPairCap]  (diag chunk: new value)
+    int* L_ph;      // [kPairCap]  batch phase of each entry
+    unsigned* bm;   // [(p + 31) / 32] row bitmap of a chunk (conflict detection)
+};
+
 __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    int2* L_rs = reinterpret_cast<int2*>(smem_raw);
-    double* L_d = reinterpret_cast<double*>(smem_raw + kCap * sizeof(int2));
-    double* D_d = reinterpret_cast<double*>(smem_raw);           // diag chunk: delta
-    double* D_new = reinterpret_cast<double*>(smem_raw) + kCap;  // diag chunk: new value
-    __shared__ int s_off[kMaxBlocks + 1];
-    __shared__ int s_cnt;
-    __shared__ double s_red[5][32];
+    __shared__ int s_epoch;               // chain: last phase g whose barrier was passed
+    __shared__ int s_staged;              // apply: highest publish phase staged
+    __shared__ int s_stop;                // chain: phase of the final diagonal step, or -1
+    __shared__ int s_stbase[kSlots];      // apply watermark each stage slot was taken at
+    __shared__ int s_cnt;                 // chain: list compaction counter
+    __shared__ int s_conflict;            // apply: a row appears twice in the current chunk
+    __shared__ int s_wsum[kApplyWarps];
+    __shared__ double s_red[4][kApplyWarps];
+    __shared__ int s_iters, s_conv;
+    __shared__ int s_aE, s_aStop;         // apply: control state broadcast by apply thread 0
+    __shared__ int s_nent, s_multi;       // apply: single-entry segments gathered / a segment had more
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b = blockIdx.x, nblk = gridDim.x;
-    const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half;
+    const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half, lmax = a.lmax;
     const int c0 = b * w;
     const int wl = min(w, p - c0);
-    const int c = c0 + tid;  // own column of a publisher thread (tid < wl)
     const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
     double* __restrict__ Wb = a.W + (long long)b * a.slab;
     const double* __restrict__ Tb = a.T + (long long)b * a.slab;
     double* __restrict__ Ob = a.Om + (long long)b * a.slab;
-    const unsigned long long nbu = (unsigned long long)nblk;
-    unsigned long long epoch = 0;
+    const int ssz = (2 + lmax) * w;  // doubles per stage slot
 
-    // ---- publish phase 0 of the first sweep, arrive
-    if (tid < wl) {
-        const int x = pub_row(0, c, m, p);
-        if (x >= 0) a.pub[c] = make_double2(Wb[(long long)x * w + tid], Ob[(long long)x * w + tid]);
+    Smem sm;
+    {
+        unsigned char* ptr = smem_raw;
+        sm.stage = reinterpret_cast<double*>(ptr);
+        ptr += sizeof(double) * (size_t)kSlots * ssz;
+        sm.L_rs = reinterpret_cast<int2*>(ptr);
+        ptr += sizeof(int2) * kPairCap;
+        sm.L_d = reinterpret_cast<double*>(ptr);
+        ptr += sizeof(double) * kPairCap;
+        sm.L_new = reinterpret_cast<double*>(ptr);
+        ptr += sizeof(double) * kPairCap;
+        sm.L_ph = reinterpret_cast<int*>(ptr);
+        ptr += sizeof(int) * kPairCap;
+        sm.s_off = reinterpret_cast<int*>(ptr);
+        ptr += sizeof(int) * ((size_t)kBatch * nblk + 1);
+        sm.bm = reinterpret_cast<unsigned*>(ptr);
     }
-    __syncthreads();
-    bar_arrive(a.bar);
-    if (b == 0 && tid == 0) a.rec_time[0] = globaltimer_ns();
+    for (int i = tid; i < (p + 31) / 32; i += kThreads) sm.bm[i] = 0u;
 
-    // ---- publisher state: cell (xp, c) for the next publish, prefetched value `pre`
-    // (W after every phase before ph0), brought forward by phases ph0 (source row y0,
-    // T[y0,c] = t0) and ph1 (y1, t1) at publish time.
-    int xp = -1, ph0 = -1, y0 = -1, ph1 = 0, y1 = -1;
-    double2 pre = make_double2(0.0, 0.0);
-    double t0 = 0.0, t1 = 0.0;
-    // prefetch for the publish done in phase `phA` (which publishes phase phA+1);
-    // `phB` is the phase before phA, or -1 when nothing precedes it.
-    auto prefetch = [&](int phB, int phA) {
-        xp = -1;
-        if (tid < wl) {
-            const int phn = (phA == m) ? 0 : phA + 1;
-            const int x = pub_row(phn, c, m, p);
-            if (x >= 0) {
-                xp = x;
-                ph0 = phB;
-                ph1 = phA;
-                y0 = (phB >= 0) ? src_row(phB, x, m) : p;
-                y1 = src_row(phA, x, m);
-                pre = make_double2(Wb[(long long)x * w + tid], Ob[(long long)x * w + tid]);
-                t0 = (y0 < p) ? __ldg(Tb + (long long)y0 * w + tid) : 0.0;
-                t1 = (y1 < p) ? __ldg(Tb + (long long)y1 * w + tid) : 0.0;
+    // ---- initial stages: publish phases 0..min(2, lmax) from the initial W (watermark -1)
+    const int init_hi = min(2, lmax);
+    for (int idx = tid; idx < (init_hi + 1) * wl; idx += kThreads) {
+        const int Q = idx / wl, j = idx - Q * wl;
+        const int phQ = Q;  // Q <= 2 <= m except when m == 1 (then lmax == 1 and Q <= 1 <= m)
+        const int x = pub_row(phQ, c0 + j, m, p);
+        double* st = sm.stage + (size_t)(Q % kSlots) * ssz;
+        if (x >= 0) {
+            st[j] = Wb[(long long)x * w + j];
+            st[w + j] = Ob[(long long)x * w + j];
+            for (int i = 0; i < Q; ++i) {  // phases k = 0 .. Q-1 not covered by the stage
+                const int y = src_row(i, x, m);
+                st[(2 + i) * w + j] = (y < p) ? __ldg(Tb + (long long)y * w + j) : 0.0;
             }
         }
-    };
-    prefetch(-1, 0);
-
-    // optional phase profile (CONCORD_PHASE_PROFILE): CTA 0 / thread 0 clock64 per phase
-    unsigned long long* prof = (a.prof && b == 0 && tid == 0) ? a.prof : nullptr;
-    long long tmark = clock64();
-#define PMARK(i)                                     \
-    if (prof) {                                      \
-        const long long t_ = clock64();              \
-        prof[i] += (unsigned long long)(t_ - tmark); \
-        tmark = t_;                                  \
     }
+    if (tid == 0) {
+        s_epoch = -1;
+        s_staged = init_hi;
+        s_stop = -1;
+        for (int i = 0; i <= init_hi; ++i) s_stbase[i] = -1;
+        s_conflict = 0;
+        s_cnt = 0;
+    }
+    __syncthreads();
 
-    int slot = 0;  // slot of the current phase; (slot+2)%3 is the previous one
-    int it = 0, converged = 0;
-    double smax = 0.0;  // max |delta| over this thread's share of the sweep
-    int snnz = 0;
-    while (true) {
-        for (int ph = 0; ph <= m; ++ph) {
-            bar_wait(a.bar, (++epoch) * nbu);
-            PMARK(0);
-            const int pslot = (slot == 0) ? 2 : slot - 1;
-            const int nslot = (slot == 2) ? 0 : slot + 1;
-            const double2* __restrict__ pb = a.pub + (size_t)slot * p;
-            const double2* __restrict__ pbm = a.pub + (size_t)pslot * p;
-            double2* __restrict__ pn = a.pub + (size_t)nslot * p;
-            const bool diag = (ph == m);
+    unsigned long long* prof = (a.prof && b == 0) ? a.prof : nullptr;
 
-            // ---- diagonal: convergence decision first (every CTA sees the same values)
+    if (warp < kChainWarps) {
+        // ============================================================ chain warps
+        const int tc = tid;
+        // initial publish (phase 0, no corrections)
+        for (int j = tc; j < wl; j += kChain)
+            if (pub_row(0, c0 + j, m, p) >= 0) a.pub[c0 + j] = make_double2(sm.stage[j], sm.stage[w + j]);
+        bar_chain();
+        if (tc == 0) {
+            __threadfence();
+            atomicAdd(a.bar, 1ull);
+        }
+        if (b == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
+
+        int g = 0, ph = 0, it = 0, converged = 0;
+        double smax = 0.0;  // max |delta| over this thread's share of the sweep
+        int snnz = 0;
+        long long t_wait = 0, t_stage = 0, t_work = 0, t_pub = 0, t_share = 0, t_end = 0;
+        while (true) {
+            long long t0 = clock64();
+            if (tc == 0) {
+                const unsigned long long target = (unsigned long long)(g + 1) * (unsigned long long)nblk;
+                while (ld_acquire_u64(a.bar) < target) {
+                }
+                st_vol(&s_epoch, g);
+            }
+            bar_chain();
+            long long t1 = clock64();
+            t_wait += t1 - t0;
+            const double2* __restrict__ pb = a.pub + (size_t)(g % 3) * p;
+            double2* __restrict__ pn = a.pub + (size_t)((g + 1) % 3) * p;
+            double* __restrict__ dg = a.dring + (size_t)(g % a.rd) * p;
+
             bool stop = false;
-            double dmax_all = 0.0;
-            if (diag) {
+            if (ph == m) {
+                // ---- diagonal step: every CTA evaluates all p closed forms (_ckernels.pyx:41-50)
+                double2* dd = a.diagd + (size_t)b * p;
                 double dm = 0.0;
-                for (int i = tid; i < p; i += kThreads)
-                    dm = fmax(dm, fabs(diag_delta(ldcg2(pb + i), __ldg(a.tdiag + i), a.n)));
+                for (int i = tc; i < p; i += kChain) {
+                    const double2 v = ldcg2(pb + i);
+                    const double nv = diag_from_dot(v.x, v.y, __ldg(a.tdiag + i), a.n);
+                    const double d = __dsub_rn(nv, v.y);
+                    dd[i] = make_double2(d, nv);
+                    if ((unsigned)(i - c0) < (unsigned)wl) dg[i] = d;
+                    dm = fmax(dm, fabs(d));
+                }
                 dm = warp_max(dm);
                 if (lane == 0) s_red[0][warp] = dm;
-                __syncthreads();
-                const double off = __longlong_as_double((long long)__ldcg(a.rec_dmax + it));
-                dmax_all = fmax(off, warp_max(lane < kThreads / 32 ? s_red[0][lane] : 0.0));
+                bar_chain();
+                double dmax_all = __longlong_as_double((long long)__ldcg(a.rec_dmax + it));
+                for (int j = 0; j < kChainWarps; ++j) dmax_all = fmax(dmax_all, s_red[0][j]);
                 stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter);
-                __syncthreads();
+                if (b == 0 && tc == 0) {
+                    a.rec_delta[it] = dmax_all;
+                    a.rec_time[it + 1] = globaltimer_ns();
+                }
+                if (stop) {
+                    converged = dmax_all < a.delta_tol;
+                    bar_chain();
+                    if (tc == 0) {
+                        __threadfence_block();
+                        s_iters = it + 1;
+                        s_conv = converged;
+                        st_vol(&s_stop, g);
+                    }
+                    break;
+                }
             }
 
-            // ---- publish phase ph+1
-            if (!stop && xp >= 0) {
-                double val = pre.x, om = pre.y, nv;
-                if (y0 < p) {
-                    const double d = row_delta(ph0, xp, y0, pbm, a.tdiag, m, a.shrink, a.n, nv);
-                    if (d != 0.0) val = fma(d, t0, val);
-                    if (y0 == c) om = nv;  // the correcting phase moved this very cell (only when m == 1)
+            // ---- publish phase g+1: staged value brought forward over the phases it misses
+            {
+                const int Q = g + 1;
+                const int phQ = (ph == m) ? 0 : ph + 1;
+                const int slot = Q % kSlots;
+                if (tc < wl) {
+                    while (ld_vol(&s_staged) < Q) {
+                    }
+                    __threadfence_block();
                 }
-                if (y1 < p) {
-                    const double d = row_delta(ph1, xp, y1, pb, a.tdiag, m, a.shrink, a.n, nv);
-                    if (d != 0.0) val = fma(d, t1, val);
-                    if (y1 == c) om = nv;
+                long long t2 = clock64();
+                t_stage += t2 - t1;
+                t1 = t2;
+                const double* st = sm.stage + (size_t)slot * ssz;
+                for (int j = tc; j < wl; j += kChain) {
+                    const int c = c0 + j;
+                    const int x = pub_row(phQ, c, m, p);
+                    if (x < 0) continue;
+                    const int C = ld_vol(&s_stbase[slot]);
+                    const int L = g - C;  // phases C+1 .. g, L >= 1
+                    double dk[kMaxLag];
+#pragma unroll
+                    for (int i = 0; i < kMaxLag; ++i) {
+                        const int k = C + 1 + i;
+                        dk[i] = (i < L - 1) ? __ldcg(a.dring + (size_t)(k % a.rd) * p + x) : 0.0;
+                    }
+                    const int y = src_row(ph, x, m);
+                    const double dlast = (y < p) ? row_delta(ph, x, y, pb, a.tdiag, m, a.shrink, a.n) : 0.0;
+                    double val = st[j];
+                    const double om = st[w + j];
+#pragma unroll
+                    for (int i = 0; i < kMaxLag; ++i)
+                        if (i < L - 1 && dk[i] != 0.0) val = fma(dk[i], st[(2 + i) * w + j], val);
+                    if (dlast != 0.0) val = fma(dlast, st[(2 + L - 1) * w + j], val);
+                    pn[c] = make_double2(val, om);
                 }
-                pn[c] = make_double2(val, om);
             }
-            PMARK(1);
 
-            // ---- share of the colour's closed forms -> list segment of this CTA
-            if (!diag) {
-                if (tid == 0) s_cnt = 0;
-                __syncthreads();
+            if (tc == 0) t_pub += clock64() - t1;
+            // ---- this CTA's share of the colour's closed forms -> dring + delta list segment
+            // (runs on the last chain threads, concurrently with the publishers above)
+            const int lslot = g % a.rl;
+            if (ph < m && b < a.nsh) {
                 const int c1 = m - 1 - ph;
-                int2* seg_rs = a.list_rs + ((size_t)slot * nblk + b) * a.share;
-                double2* seg_dn = a.list_dn + ((size_t)slot * nblk + b) * a.share;
-                const int sid = kThreads - 1 - tid;  // share work starts on the last warps
-                for (int base = q_lo; base < q_hi; base += kThreads) {
+                int2* seg_rs = a.list_rs + ((size_t)lslot * nblk + b) * a.share;
+                double2* seg_dn = a.list_dn + ((size_t)lslot * nblk + b) * a.share;
+                const int sid = kChain - 1 - tc;  // share work starts on the last chain warps
+                for (int base = q_lo; base < q_hi; base += kChain) {
                     const int q = base + sid;
                     int r = 0, s = 0;
                     double d = 0.0, nv = 0.0;
@@ -257,10 +397,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         if (s < p) {
                             d = pair_delta(ldcg2(pb + r), ldcg2(pb + s), __ldg(a.tdiag + r), __ldg(a.tdiag + s),
                                            a.shrink, nv);
+                            dg[r] = d;
+                            dg[s] = d;
                             if (d != 0.0) {
                                 smax = fmax(smax, fabs(d));
                                 ++snnz;
                             }
+                        } else {
+                            dg[r] = 0.0;  // partner is the phantom (odd p)
                         }
                     }
                     const unsigned mask = __ballot_sync(0xffffffffu, d != 0.0);
@@ -275,231 +419,357 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         }
                     }
                 }
-                __syncthreads();
-                if (tid == 0) a.list_cnt[(size_t)slot * nblk + b] = s_cnt;
-                if (ph == m - 1) {  // flush this sweep's share statistics
+                if (ph == m - 1) {  // this sweep's share statistics: per-warp partials
                     const double mw = warp_max(smax);
                     const double nw = warp_sum((double)snnz);
                     if (lane == 0) {
                         s_red[0][warp] = mw;
                         s_red[1][warp] = nw;
                     }
-                    __syncthreads();
-                    if (warp == 0) {
-                        const bool in = lane < kThreads / 32;
-                        const double mb = warp_max(in ? s_red[0][lane] : 0.0);
-                        const double nbk = warp_sum(in ? s_red[1][lane] : 0.0);
-                        if (lane == 0) {
-                            atomicMax(a.rec_dmax + it, (unsigned long long)__double_as_longlong(mb));
-                            atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + it),
-                                      (unsigned long long)nbk);
-                        }
-                    }
                     smax = 0.0;
                     snnz = 0;
                 }
             }
-            PMARK(2);
-            if (!stop) {
-                __syncthreads();
-                bar_arrive(a.bar);
-            }
-
-            // ---- apply the previous colour's non-zero deltas to the own slab
-            const int prev = (ph == 0) ? -1 : ph - 1;  // phase 0 follows the diagonal (already applied)
-            if (prev >= 0 && (it > 0 || ph > 0)) {
-                for (int j = tid; j < nblk; j += kThreads) s_off[j] = __ldcg(a.list_cnt + (size_t)pslot * nblk + j);
-                __syncthreads();
-                if (warp == 0) {
-                    int run = 0;
-                    for (int j0 = 0; j0 < nblk; j0 += 32) {
-                        const int j = j0 + lane;
-                        int v = (j < nblk) ? s_off[j] : 0;
-                        int incl = v;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += t;
-                        }
-                        if (j < nblk) s_off[j] = run + incl - v;
-                        run += __shfl_sync(0xffffffffu, incl, 31);
-                    }
-                    if (lane == 0) s_off[nblk] = run;
+            if (tc == kChain - 1) t_share += clock64() - t1;
+            const long long tb = clock64();
+            bar_chain();
+            if (tc == 0) {
+                if (ph < m && b < a.nsh) {
+                    a.list_cnt[(size_t)lslot * nblk + b] = s_cnt;
+                    s_cnt = 0;
                 }
-                __syncthreads();
-                const int total = s_off[nblk];
-                const int2* lrs = a.list_rs + (size_t)pslot * nblk * a.share;
-                const double2* ldn = a.list_dn + (size_t)pslot * nblk * a.share;
-                for (int e0 = 0; e0 < total; e0 += kCap) {
-                    const int e1 = min(total, e0 + kCap);
-                    for (int e = e0 + tid; e < e1; e += kThreads) {
-                        int lo = 0, hi = nblk;  // segment: s_off[lo] <= e < s_off[lo+1]
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (s_off[mid] <= e) lo = mid;
-                            else hi = mid;
-                        }
-                        const size_t at = (size_t)lo * a.share + (e - s_off[lo]);
-                        const int2 rs = __ldcg(lrs + at);
-                        const double2 dn = __ldcg(ldn + at);
-                        if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
-                        if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
-                        L_rs[e - e0] = rs;
-                        L_d[e - e0] = dn.x;
+                if (ph == m - 1 && b < a.nsh) {
+                    double mb = 0.0, nbk = 0.0;
+                    for (int j = 0; j < kChainWarps; ++j) {
+                        mb = fmax(mb, s_red[0][j]);
+                        nbk += s_red[1][j];
                     }
-                    __syncthreads();
-                    const int per = 2 * w2;
-                    const int items = (e1 - e0) * per;
-                    for (int base = 0; base < items; base += kThreads * kUnroll) {
-                        double2 tv[kUnroll], wv[kUnroll];
-                        double2* wp[kUnroll];
-                        double dd[kUnroll];
-#pragma unroll
-                        for (int u = 0; u < kUnroll; ++u) {
-                            const int idx = base + u * kThreads + tid;
-                            wp[u] = nullptr;
-                            if (idx < items) {
-                                const int e = idx / per;
-                                const int rem = idx - e * per;
-                                const int h = rem >= w2;
-                                const int j2 = rem - h * w2;
-                                const int2 rs = L_rs[e];
-                                dd[u] = L_d[e];
-                                const int dst = h ? rs.y : rs.x;
-                                const int src = h ? rs.x : rs.y;
-                                wp[u] = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
-                                tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
-                                wv[u] = *wp[u];
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < kUnroll; ++u) {
-                            if (wp[u]) {
-                                wv[u].x = fma(dd[u], tv[u].x, wv[u].x);
-                                wv[u].y = fma(dd[u], tv[u].y, wv[u].y);
-                                *wp[u] = wv[u];
-                            }
-                        }
-                    }
-                    __syncthreads();
+                    atomicMax(a.rec_dmax + it, (unsigned long long)__double_as_longlong(mb));
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + it), (unsigned long long)nbk);
                 }
+                __threadfence();
+                atomicAdd(a.bar, 1ull);
             }
-            PMARK(3);
-
-            if (!diag) {
-                prefetch(ph, ph + 1);
-                PMARK(4);
-                slot = nslot;
+            if (tc == 0) t_end += clock64() - tb;
+            t_work += clock64() - t1;
+            if (ph == m) {
+                ph = 0;
+                ++it;
+            } else {
+                ++ph;
+            }
+            ++g;
+        }
+        if (prof && tc == 0) {
+            prof[0] = (unsigned long long)t_wait;
+            prof[1] = (unsigned long long)t_stage;
+            prof[2] = (unsigned long long)t_work;
+            prof[3] = (unsigned long long)g;
+            prof[7] = (unsigned long long)t_pub;
+            prof[8] = (unsigned long long)t_end;
+        }
+        if (prof && tc == kChain - 1) {
+            prof[9] = (unsigned long long)t_share;
+        }
+    } else {
+        // ============================================================ apply warps
+        const int ta = tid - kChain;
+        int C = -1;            // every phase <= C is in the own slab
+        int cph = m;           // phase-in-sweep of C (C = -1 behaves like a diagonal step)
+        int cit = -1;          // sweep of C
+        int staged = init_hi;  // highest publish phase staged
+        int nbmax = kBatch;    // phases per batch (1 after a dense batch)
+        long long t_busy = 0, t_idle = 0, nbatch = 0, t_head = 0, t_diag = 0;
+        while (true) {
+            const long long t0 = clock64();
+            bar_apply();  // everyone has consumed the previous broadcast
+            if (ta == 0) {
+                s_aE = ld_vol(&s_epoch);
+                s_aStop = ld_vol(&s_stop);
+                s_nent = 0;
+                s_multi = 0;
+                s_conflict = 0;
+                __threadfence_block();
+            }
+            bar_apply();
+            const int E = s_aE;
+            const int stopg = s_aStop;
+            const int avail = (stopg >= 0) ? stopg : E - 1;  // phases whose deltas are all visible
+            const int k0 = C + 1;
+            const int ph0 = (cph == m) ? 0 : cph + 1;
+            const int it0 = (cph == m) ? cit + 1 : cit;
+            const bool have = C < avail;
+            const bool diag = have && ph0 == m;
+            const int k1 = (have && !diag) ? min(min(avail, k0 + nbmax - 1), k0 + (m - 1 - ph0)) : C;
+            const int nb = k1 - C;  // colour phases in this batch (0 for none / diagonal)
+            const int nsh = a.nsh;
+            const int nseg = nb * nsh;
+            // stage with the pre-batch watermark C: the publish corrections cover this batch too
+            const int target = (stopg < 0) ? min(E + a.stage_ahead, C + 1 + lmax) : staged;
+            const int nq = max(0, target - staged);
+            if (!have && nq == 0) {
+                t_idle += clock64() - t0;
+                __nanosleep(32);
                 continue;
             }
 
-            // ---- diagonal step: prefetch (W before this phase), then the dense slab stream
-            if (!stop) prefetch(m, 0);
-            double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
-            for (int i0 = 0; i0 < p; i0 += kCap) {
-                const int iend = min(i0 + kCap, p);
-                for (int i = i0 + tid; i < iend; i += kThreads) {
-                    const double2 v = ldcg2(pb + i);
-                    const double nv = diag_from_dot(v.x, v.y, __ldg(a.tdiag + i), a.n);
-                    D_d[i - i0] = __dsub_rn(nv, v.y);
-                    D_new[i - i0] = nv;
-                }
-                __syncthreads();
-                const int items = (iend - i0) * w2;
-                for (int base = 0; base < items; base += kThreads * kUnroll) {
-                    double2 wv[kUnroll], tv[kUnroll], ov[kUnroll];
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u) {
-                        const int idx = base + u * kThreads + tid;
-                        if (idx < items) {
-                            const int ii = idx / w2;
-                            const int j2 = idx - ii * w2;
-                            const long long off = (long long)(i0 + ii) * w + 2 * j2;
-                            wv[u] = *reinterpret_cast<const double2*>(Wb + off);
-                            if (D_d[ii] != 0.0) tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + off));
-                            if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
-                        }
+            // ---- one round trip: segment heads (count + first entry) and the stage cells
+            for (int idx = ta; idx < nseg; idx += kApply) {
+                const int jb = idx / nsh;
+                const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
+                const int cnt = __ldcg(a.list_cnt + seg);
+                const int2 rs = __ldcg(a.list_rs + (size_t)seg * a.share);
+                const double2 dn = __ldcg(a.list_dn + (size_t)seg * a.share);
+                sm.s_off[idx] = cnt;
+                if (cnt > 1) s_multi = 1;
+                if (cnt == 1) {
+                    const int pos = atomicAdd(&s_nent, 1);
+                    if (pos < kPairCap) {
+                        sm.L_rs[pos] = rs;
+                        sm.L_d[pos] = dn.x;
+                        sm.L_ph[pos] = jb;
+                    } else {
+                        s_multi = 1;
                     }
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u) {
-                        const int idx = base + u * kThreads + tid;
-                        if (idx < items) {
-                            const int ii = idx / w2;
-                            const int j2 = idx - ii * w2;
-                            const int i = i0 + ii;
-                            const long long off = (long long)i * w + 2 * j2;
-                            const double d = D_d[ii];
-                            if (d != 0.0) {
-                                wv[u].x = fma(d, tv[u].x, wv[u].x);
-                                wv[u].y = fma(d, tv[u].y, wv[u].y);
-                                *reinterpret_cast<double2*>(Wb + off) = wv[u];
-                            }
-                            const int cj = c0 + 2 * j2;
-                            const bool dg0 = (cj == i), dg1 = (cj + 1 == i);
-                            if (a.want_trace) {
-                                if (dg0 | dg1) {
-                                    if (dg0) ov[u].x = D_new[ii];
-                                    if (dg1) ov[u].y = D_new[ii];
-                                    *reinterpret_cast<double2*>(Ob + off) = ov[u];
-                                    log_acc += log(D_new[ii]);
-                                }
-                                q_acc = fma(wv[u].x, ov[u].x, q_acc);
-                                q_acc = fma(wv[u].y, ov[u].y, q_acc);
-                                if (i < cj) pen_acc += fabs(ov[u].x);
-                                if (i < cj + 1) pen_acc += fabs(ov[u].y);
-                            } else if (dg0 | dg1) {
-                                Ob[off + (dg0 ? 0 : 1)] = D_new[ii];
-                            }
-                        }
-                    }
+                    if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
+                    if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
                 }
-                __syncthreads();
             }
-            ++it;
-            PMARK(5);
+            for (int idx = ta; idx < nq * wl; idx += kApply) {
+                const int qi = idx / wl, j = idx - qi * wl;
+                const int Q = staged + 1 + qi;
+                const int x = pub_row(Q % (m + 1), c0 + j, m, p);
+                if (x < 0) continue;
+                double* st = sm.stage + (size_t)(Q % kSlots) * ssz;
+                const int L = Q - 1 - C;
+                double tv[kMaxLag];
+                int phk = ph0;  // phase-in-sweep of C+1
+#pragma unroll
+                for (int i = 0; i < kMaxLag; ++i) {
+                    const int y = src_row(phk, x, m);
+                    tv[i] = (i < L && y < p) ? __ldg(Tb + (long long)y * w + j) : 0.0;
+                    phk = (phk == m) ? 0 : phk + 1;
+                }
+                const double wv = Wb[(long long)x * w + j];
+                const double ov = Ob[(long long)x * w + j];
+                st[j] = wv;
+                st[w + j] = ov;
+#pragma unroll
+                for (int i = 0; i < kMaxLag; ++i)
+                    if (i < L) st[(2 + i) * w + j] = tv[i];
+            }
+            for (int Q = staged + 1 + ta; Q <= target; Q += kApply) s_stbase[Q % kSlots] = C;
+            bar_apply();
+            t_head += clock64() - t0;
+            if (nq > 0) {
+                staged = target;
+                if (ta == 0) {
+                    __threadfence_block();
+                    st_vol(&s_staged, staged);
+                }
+            }
 
-            // ---- per-sweep records
-            q_acc = warp_sum(q_acc);
-            pen_acc = warp_sum(pen_acc);
-            log_acc = warp_sum(log_acc);
-            if (lane == 0) {
-                s_red[1][warp] = q_acc;
-                s_red[2][warp] = pen_acc;
-                s_red[3][warp] = log_acc;
-            }
-            __syncthreads();
-            if (warp == 0) {
-                const bool in = lane < kThreads / 32;
-                const double v1 = warp_sum(in ? s_red[1][lane] : 0.0);
-                const double v2 = warp_sum(in ? s_red[2][lane] : 0.0);
-                const double v3 = warp_sum(in ? s_red[3][lane] : 0.0);
-                if (lane == 0) {
-                    if (a.want_trace) {
-                        double* ro = a.rec_obj + ((size_t)(it - 1) * nblk + b) * 3;
+            if (diag) {
+                // ---- dense diagonal step over the own slab (+ objective records)
+                const double2* dd = a.diagd + (size_t)b * p;
+                double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
+                for (int i0 = 0; i0 < p; i0 += kPairCap) {
+                    const int iend = min(i0 + kPairCap, p);
+                    for (int i = i0 + ta; i < iend; i += kApply) {
+                        const double2 v = ldcg2(dd + i);
+                        sm.L_d[i - i0] = v.x;
+                        sm.L_new[i - i0] = v.y;
+                    }
+                    bar_apply();
+                    const int items = (iend - i0) * w2;
+                    for (int base = 0; base < items; base += kApply * kUnroll) {
+                        double2 wv[kUnroll], tv[kUnroll], ov[kUnroll];
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int idx = base + u * kApply + ta;
+                            if (idx < items) {
+                                const int ii = idx / w2;
+                                const int j2 = idx - ii * w2;
+                                const long long off = (long long)(i0 + ii) * w + 2 * j2;
+                                wv[u] = *reinterpret_cast<const double2*>(Wb + off);
+                                if (sm.L_d[ii] != 0.0) tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + off));
+                                if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int idx = base + u * kApply + ta;
+                            if (idx < items) {
+                                const int ii = idx / w2;
+                                const int j2 = idx - ii * w2;
+                                const int i = i0 + ii;
+                                const long long off = (long long)i * w + 2 * j2;
+                                const double d = sm.L_d[ii];
+                                if (d != 0.0) {
+                                    wv[u].x = fma(d, tv[u].x, wv[u].x);
+                                    wv[u].y = fma(d, tv[u].y, wv[u].y);
+                                    *reinterpret_cast<double2*>(Wb + off) = wv[u];
+                                }
+                                const int cj = c0 + 2 * j2;
+                                const bool dg0 = (cj == i), dg1 = (cj + 1 == i);
+                                if (a.want_trace) {
+                                    if (dg0 | dg1) {
+                                        if (dg0) ov[u].x = sm.L_new[ii];
+                                        if (dg1) ov[u].y = sm.L_new[ii];
+                                        *reinterpret_cast<double2*>(Ob + off) = ov[u];
+                                        log_acc += log(sm.L_new[ii]);
+                                    }
+                                    q_acc = fma(wv[u].x, ov[u].x, q_acc);
+                                    q_acc = fma(wv[u].y, ov[u].y, q_acc);
+                                    if (i < cj) pen_acc += fabs(ov[u].x);
+                                    if (i < cj + 1) pen_acc += fabs(ov[u].y);
+                                } else if (dg0 | dg1) {
+                                    Ob[off + (dg0 ? 0 : 1)] = sm.L_new[ii];
+                                }
+                            }
+                        }
+                    }
+                    bar_apply();
+                }
+                if (a.want_trace) {
+                    q_acc = warp_sum(q_acc);
+                    pen_acc = warp_sum(pen_acc);
+                    log_acc = warp_sum(log_acc);
+                    const int wa = ta >> 5;
+                    if (lane == 0) {
+                        s_red[1][wa] = q_acc;
+                        s_red[2][wa] = pen_acc;
+                        s_red[3][wa] = log_acc;
+                    }
+                    bar_apply();
+                    if (ta == 0) {
+                        double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                        for (int j = 0; j < kApplyWarps; ++j) {
+                            v1 += s_red[1][j];
+                            v2 += s_red[2][j];
+                            v3 += s_red[3][j];
+                        }
+                        double* ro = a.rec_obj + ((size_t)it0 * nblk + b) * 3;
                         ro[0] = v1;
                         ro[1] = v2;
                         ro[2] = v3;
                     }
-                    if (b == 0) {
-                        a.rec_delta[it - 1] = dmax_all;
-                        a.rec_time[it] = globaltimer_ns();
+                }
+                C = k0;
+                cph = m;
+                cit = it0;
+                t_diag += clock64() - t0;
+            } else if (nb > 0) {
+                // ---- colour phases k0 .. k1
+                int total = 0;
+                if (!s_multi) {
+                    // every segment had at most one entry: they are already in shared memory
+                    const int nent = s_nent;
+                    if (nb > 1) {
+                        for (int e = ta; e < nent; e += kApply) {
+                            const int2 rs = sm.L_rs[e];
+                            const unsigned br = 1u << (rs.x & 31), bs = 1u << (rs.y & 31);
+                            const unsigned o1 = atomicOr(sm.bm + (rs.x >> 5), br);
+                            const unsigned o2 = atomicOr(sm.bm + (rs.y >> 5), bs);
+                            if ((o1 & br) | (o2 & bs)) s_conflict = 1;
+                        }
+                        bar_apply();
+                    }
+                    if (!s_conflict) {
+                        apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, nent, w2, Wb, Tb, ta);
+                    } else {
+                        for (int jb = 0; jb < nb; ++jb) {  // rows repeat across phases: phase by phase
+                            apply_rows(sm.L_rs, sm.L_d, sm.L_ph, jb, 0, nent, w2, Wb, Tb, ta);
+                            bar_apply();
+                        }
+                    }
+                    bar_apply();
+                    if (nb > 1) {
+                        for (int e = ta; e < nent; e += kApply) {
+                            const int2 rs = sm.L_rs[e];
+                            atomicAnd(sm.bm + (rs.x >> 5), ~(1u << (rs.x & 31)));
+                            atomicAnd(sm.bm + (rs.y >> 5), ~(1u << (rs.y & 31)));
+                        }
+                    }
+                    total = nent;
+                } else {
+                    // general path: exclusive scan of the segment counts, entries in phase order
+                    total = apply_scan(sm.s_off, nseg, ta, s_wsum);
+                    for (int e0 = 0; e0 < total; e0 += kPairCap) {
+                        const int e1 = min(total, e0 + kPairCap);
+                        for (int e = e0 + ta; e < e1; e += kApply) {
+                            int lo = 0, hi = nseg;  // segment: s_off[lo] <= e < s_off[lo+1]
+                            while (hi - lo > 1) {
+                                const int mid = (lo + hi) >> 1;
+                                if (sm.s_off[mid] <= e) lo = mid;
+                                else hi = mid;
+                            }
+                            const int jb = lo / nsh;
+                            const int rank = e - sm.s_off[lo];
+                            const size_t at =
+                                ((size_t)((k0 + jb) % a.rl) * nblk + (lo - jb * nsh)) * a.share + rank;
+                            const int2 rs = __ldcg(a.list_rs + at);
+                            const double2 dn = __ldcg(a.list_dn + at);
+                            // segments with one entry had their Omega cells written above
+                            if (sm.s_off[lo + 1] - sm.s_off[lo] > 1) {
+                                if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
+                                if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                            }
+                            sm.L_rs[e - e0] = rs;
+                            sm.L_d[e - e0] = dn.x;
+                            sm.L_ph[e - e0] = jb;
+                            if (nb > 1) {
+                                const unsigned br = 1u << (rs.x & 31), bs = 1u << (rs.y & 31);
+                                const unsigned o1 = atomicOr(sm.bm + (rs.x >> 5), br);
+                                const unsigned o2 = atomicOr(sm.bm + (rs.y >> 5), bs);
+                                if ((o1 & br) | (o2 & bs)) s_conflict = 1;
+                            }
+                        }
+                        bar_apply();
+                        const int conflict = s_conflict;
+                        if (!conflict) {
+                            apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, e1 - e0, w2, Wb, Tb, ta);
+                        } else {
+                            for (int jb = 0; jb < nb; ++jb) {
+                                const int lo = max(sm.s_off[jb * nsh], e0) - e0;
+                                const int hi = min(sm.s_off[(jb + 1) * nsh], e1) - e0;
+                                if (lo < hi) apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, lo, hi, w2, Wb, Tb, ta);
+                                bar_apply();
+                            }
+                        }
+                        bar_apply();
+                        if (nb > 1) {
+                            for (int e = ta; e < e1 - e0; e += kApply) {
+                                const int2 rs = sm.L_rs[e];
+                                atomicAnd(sm.bm + (rs.x >> 5), ~(1u << (rs.x & 31)));
+                                atomicAnd(sm.bm + (rs.y >> 5), ~(1u << (rs.y & 31)));
+                            }
+                        }
+                        bar_apply();
+                        if (ta == 0) s_conflict = 0;
                     }
                 }
+                nbmax = (total > 256) ? 1 : kBatch;
+                C = k1;
+                cph = ph0 + (k1 - k0);
+                cit = it0;
+                ++nbatch;
             }
-            __syncthreads();
-            PMARK(6);
-            if (stop) {
-                converged = dmax_all < a.delta_tol;
-                break;
-            }
-            slot = nslot;
+            t_busy += clock64() - t0;
+            if (stopg >= 0 && C >= stopg) break;
         }
-        if (it > 0 && (converged || it >= a.max_iter)) break;
+        if (prof && ta == 0) {
+            prof[4] = (unsigned long long)t_busy;
+            prof[5] = (unsigned long long)t_idle;
+            prof[6] = (unsigned long long)nbatch;
+            prof[10] = (unsigned long long)t_head;
+            prof[11] = (unsigned long long)t_diag;
+        }
     }
-#undef PMARK
+    __syncthreads();
     if (b == 0 && tid == 0) {
-        a.status[0] = it;
-        a.status[1] = converged;
+        a.status[0] = s_iters;
+        a.status[1] = s_conv;
     }
 }
 
@@ -587,9 +857,25 @@ __global__ void wform_init_csr_kernel(const int* __restrict__ rowptr, const int*
     }
 }
 
+
 // ------------------------------------------------------------------ launchers
+int wform_lag_cap(int w, int m) {
+    int l = WFORM_MAX_LAG < m ? WFORM_MAX_LAG : m;
+    while (l > 1 && (size_t)kSlots * (2 + l) * w * sizeof(double) > 150 * 1024) --l;
+    return l;
+}
+
+size_t wform_smem_bytes(int w, int p, int nblk, int lmax) {
+    size_t b = sizeof(double) * (size_t)kSlots * (2 + lmax) * w;
+    b += (sizeof(int2) + 2 * sizeof(double) + sizeof(int)) * kPairCap;
+    b += sizeof(int) * ((size_t)kBatch * nblk + 1);
+    b = (b + 15) & ~(size_t)15;
+    b += sizeof(unsigned) * (size_t)((p + 31) / 32);
+    return b;
+}
+
 cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st) {
-    const size_t smem = wform_smem_bytes(args.w);
+    const size_t smem = wform_smem_bytes(args.w, args.p, nblk, args.lmax);
     cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -598,8 +884,9 @@ cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st) {
     return cudaLaunchCooperativeKernel((void*)pcd_wform_kernel, dim3(nblk), dim3(kThreads), kargs, smem, st);
 }
 
-cudaError_t wform_max_blocks(int w, int* max_blocks) {
-    const size_t smem = wform_smem_bytes(w);
+cudaError_t wform_max_blocks(int w, int p, int* max_blocks) {
+    const int nblk = (p + w - 1) / w;
+    const size_t smem = wform_smem_bytes(w, p, nblk, wform_lag_cap(w, p + (p & 1) - 1));
     cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
