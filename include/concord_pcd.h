@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CONCORD_ABI_VERSION 1
+#define CONCORD_ABI_VERSION 2
 
 /* Return codes. */
 #define CONCORD_OK 0
@@ -44,6 +44,23 @@ extern "C" {
 #define CONCORD_DEVICE 1
 
 typedef struct concord_solver concord_solver;
+
+/* Bytes of one shard's exported exchange-buffer handle (a cudaIpcMemHandle_t). */
+#define CONCORD_SHARD_HANDLE_BYTES 64
+
+/* Column partition of a solver (or of one shard of a multi-GPU solver). */
+typedef struct {
+    int64_t p;
+    int32_t slab_width;       /* columns per CTA                                            */
+    int32_t n_shards;         /* GPUs (or virtual shards) the columns are split over        */
+    int32_t rank;             /* this process's shard, -1 when every shard is local         */
+    int32_t blocks_per_shard; /* CTAs (column slabs) per shard                              */
+    int32_t blocks_total;
+    int64_t col0;             /* first column this solver holds                             */
+    int64_t ncols;            /* columns this solver holds (p unless it is one shard)       */
+    int32_t lag_cap;          /* phases the apply warps may trail the colour chain          */
+    int32_t reserved;
+} concord_layout;
 
 typedef struct {
     double lam;          /* penalty; the soft threshold is n*lam (solver.py:285)           */
@@ -75,6 +92,24 @@ int concord_device_count(int* count);
 /* n_blocks: 0 = automatic slab count; otherwise the number of column slabs. */
 int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_solver** out);
 int concord_solver_destroy(concord_solver* s);
+/* The same solver with its columns split over n_shards virtual shards on ONE
+ * device: every exchange buffer is replicated n_shards times and written by
+ * all shards, exactly as the multi-GPU solver does over NVLink.
+ * Results are bitwise identical for every n_shards. */
+int concord_solver_create_sharded(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
+                                  concord_solver** out);
+int concord_solver_layout(concord_solver* s, concord_layout* out);
+
+/* ---- multi-GPU: one process per GPU, column-sharded --------- */
+/* Shard `rank` of n_shards.  Exchange the handles (all-gather of
+ * CONCORD_SHARD_HANDLE_BYTES per rank, rank order) and open the peers before
+ * the first fit; every rank then calls concord_solver_fit concurrently.
+ * set_gram / gram_from_data take the FULL T / X; get_omega / get_gram return
+ * this shard's p x ncols column block (concord_solver_layout). */
+int concord_shard_create(int64_t p, int32_t n_shards, int32_t rank, int32_t device, int32_t n_blocks,
+                         concord_solver** out);
+int concord_shard_ipc_handle(concord_solver* s, void* handle_out);
+int concord_shard_open_peers(concord_solver* s, const void* handles);
 /* Use a caller stream (cudaStream_t as void*); NULL restores the solver's own. */
 int concord_solver_set_stream(concord_solver* s, void* stream);
 void* concord_solver_stream(concord_solver* s);
@@ -89,6 +124,10 @@ int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where);
 int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord_fit_result* res,
                        double* delta_trace, double* objective_trace, double* sweep_seconds);
 int concord_solver_get_omega(concord_solver* s, double* omega_out, int32_t where);
+/* Per-sweep objective partial sums of this solver's columns for the last fit:
+ * parts[3*i .. 3*i+2] = (<W,Omega>, sum_{i<j}|omega_ij|, sum log omega_ii)
+ * (a shard's partials add up across shards). */
+int concord_solver_objective_parts(concord_solver* s, double* parts, int32_t cap);
 int concord_solver_edge_count(concord_solver* s, int64_t* out);
 /* Non-zero off-diagonal deltas of each sweep of the last fit (the row streams
  * the kernel applied; used for the roofline's algorithmic bytes).  Copies

@@ -9,7 +9,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libconcord_b200.so")
+LIB_PATH = os.environ.get("CONCORD_LIB_PATH") or os.path.join(PKG, "libconcord_b200.so")
 
 CONCORD_OK = 0
 CONCORD_ERR_ARG = -1
@@ -29,7 +29,12 @@ EXPORTS = (
     "concord_solver_edge_count", "concord_solver_sweep_stats", "concord_host_alloc",
     "concord_host_free", "concord_gram_f64", "concord_pcd_fit",
     "concord_pcd_sweep_exact", "concord_u2_sweep_exact", "concord_cd_sweep_exact",
+    "concord_solver_create_sharded", "concord_solver_layout", "concord_shard_create",
+    "concord_shard_ipc_handle", "concord_shard_open_peers", "concord_solver_objective_parts",
 )
+
+ABI_VERSION = 2
+SHARD_HANDLE_BYTES = 64
 
 
 class FitParams(ctypes.Structure):
@@ -54,6 +59,21 @@ class FitResult(ctypes.Structure):
         ("setup_ms", ctypes.c_double),
         ("n_blocks", ctypes.c_int32),
         ("slab_width", ctypes.c_int32),
+    ]
+
+
+class Layout(ctypes.Structure):
+    _fields_ = [
+        ("p", ctypes.c_int64),
+        ("slab_width", ctypes.c_int32),
+        ("n_shards", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("blocks_per_shard", ctypes.c_int32),
+        ("blocks_total", ctypes.c_int32),
+        ("col0", ctypes.c_int64),
+        ("ncols", ctypes.c_int64),
+        ("lag_cap", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -108,6 +128,12 @@ def load(build_if_missing=True):
             "concord_pcd_sweep_exact": ([vp, vp, i64, d, d, vp, vp, vp, i64, i32], ctypes.c_int),
             "concord_u2_sweep_exact": ([vp, vp, i64, d, d, vp, vp, i64, i32], ctypes.c_int),
             "concord_cd_sweep_exact": ([vp, vp, i64, d, d, i32], ctypes.c_int),
+            "concord_solver_create_sharded": ([i64, i32, i32, i32, ctypes.POINTER(vp)], ctypes.c_int),
+            "concord_solver_layout": ([vp, ctypes.POINTER(Layout)], ctypes.c_int),
+            "concord_shard_create": ([i64, i32, i32, i32, i32, ctypes.POINTER(vp)], ctypes.c_int),
+            "concord_shard_ipc_handle": ([vp, vp], ctypes.c_int),
+            "concord_shard_open_peers": ([vp, vp], ctypes.c_int),
+            "concord_solver_objective_parts": ([vp, vp, i32], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -1,9 +1,9 @@
 // extern "C" ABI of libconcord_b200.so (include/concord_pcd.h).
 #include <cuda_runtime.h>
 #include <math.h>
-#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -64,14 +64,48 @@ int check_device(int32_t device) {
     return CONCORD_OK;
 }
 
+// Byte offsets of the exchange buffers inside one arena (identical on every shard).
+struct ArenaLayout {
+    size_t pub, dring, list_rs, list_dn, list_cnt, bar, dmax, bytes;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+ArenaLayout arena_layout(int p, int rd, int rl, int nblk_tot, int share) {
+    ArenaLayout L;
+    size_t o = 0;
+    L.pub = o;
+    o = align256(o + sizeof(double2) * 3 * (size_t)p);
+    L.dring = o;
+    o = align256(o + sizeof(double) * (size_t)rd * p);
+    L.list_rs = o;
+    o = align256(o + sizeof(int2) * (size_t)rl * nblk_tot * share);
+    L.list_dn = o;
+    o = align256(o + sizeof(double2) * (size_t)rl * nblk_tot * share);
+    L.list_cnt = o;
+    o = align256(o + sizeof(int) * (size_t)rl * nblk_tot);
+    L.bar = o;
+    o = align256(o + sizeof(unsigned long long));
+    L.dmax = o;
+    o = align256(o + sizeof(unsigned long long) * WFORM_DMAX_RING);
+    L.bytes = o;
+    return L;
+}
+
 }  // namespace
 
 struct concord_solver {
     int dev = 0;
     int p = 0;
     int w = 0;
-    int nblk = 0;
+    int G = 1;            // shards
+    int rank = -1;        // -1: every shard on this device; else the one shard this process owns
+    int nblk_loc = 0;     // slabs per shard
+    int nblk_tot = 0;     // slabs over all shards
+    int blk0 = 0;         // first global slab of this solver's launch
+    int nblk_launch = 0;  // slabs (CTAs) this solver launches
     long long slab = 0;
+    int lmax = 1, rd = 0, rl = 0, share = 0, nsh = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     double* T = nullptr;
@@ -79,26 +113,20 @@ struct concord_solver {
     double* Om = nullptr;
     double* tdiag = nullptr;
     double* stage = nullptr;  // p x p row-major scratch (lazy)
-    double2* pub = nullptr;
-    unsigned long long* bar = nullptr;
+    double2* diagd = nullptr;
+    ArenaLayout L{};
+    void* arena[WFORM_MAX_SHARDS] = {};
+    bool arena_owned[WFORM_MAX_SHARDS] = {};
+    bool peers_open = false;
+    unsigned long long bar_base = 0;  // barrier arrivals so far (identical on every shard)
+    int it_base = 0;                  // sweeps run so far (identical on every shard)
     unsigned long long* edges = nullptr;
     int* status = nullptr;
     double* rec_delta = nullptr;
     double* rec_obj = nullptr;
     unsigned long long* rec_time = nullptr;
     long long* rec_nnz = nullptr;
-    unsigned long long* rec_dmax = nullptr;
     int rec_cap = 0;
-    int share = 0;
-    int nsh = 0;
-    int lmax = 1;
-    int rd = 0;
-    int rl = 0;
-    double* dring = nullptr;
-    double2* diagd = nullptr;
-    int2* list_rs = nullptr;
-    double2* list_dn = nullptr;
-    int* list_cnt = nullptr;
     int last_iters = 0;
     int* csr_rowptr = nullptr;
     int* csr_col = nullptr;
@@ -122,23 +150,36 @@ int ensure_records(concord_solver* s, int cap) {
     cudaFree(s->rec_obj);
     cudaFree(s->rec_time);
     cudaFree(s->rec_nnz);
-    cudaFree(s->rec_dmax);
-    s->rec_dmax = nullptr;
     s->rec_delta = nullptr;
     s->rec_obj = nullptr;
     s->rec_time = nullptr;
     s->rec_nnz = nullptr;
     CK(dalloc(&s->rec_delta, cap));
     CK(dalloc(&s->rec_nnz, cap));
-    CK(dalloc(&s->rec_dmax, cap));
-    CK(dalloc(&s->rec_obj, (size_t)cap * s->nblk * 3));
+    CK(dalloc(&s->rec_obj, (size_t)cap * s->nblk_launch * 3));
     CK(dalloc(&s->rec_time, cap + 1));
     s->rec_cap = cap;
     return CONCORD_OK;
 }
 
-int finish_gram(concord_solver* s) {
-    CK(launch_slab_diag(s->T, s->tdiag, s->p, s->w, s->stream));
+int ncols_local(const concord_solver* s) {
+    const int c0 = s->blk0 * s->w;
+    const int c1 = (s->blk0 + s->nblk_launch) * s->w;
+    return (c1 < s->p ? c1 : s->p) - (c0 < s->p ? c0 : s->p);
+}
+
+// Row-major p x p (host or device) -> this solver's T slabs and the replicated diagonal.
+int set_gram_rowmajor(concord_solver* s, const double* src, int32_t where) {
+    const double* dsrc = src;
+    if (where == CONCORD_HOST) {
+        int rc = ensure_stage(s);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(s->stage, src, sizeof(double) * (size_t)s->p * s->p, cudaMemcpyHostToDevice,
+                           s->stream));
+        dsrc = s->stage;
+    }
+    CK(launch_pack_slabs(dsrc, s->p, s->T, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
+    CK(launch_rowmajor_diag(dsrc, s->tdiag, s->p, s->stream));
     std::vector<double> d(s->p);
     CK(cudaMemcpyAsync(d.data(), s->tdiag, sizeof(double) * s->p, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
@@ -151,35 +192,22 @@ int finish_gram(concord_solver* s) {
     return CONCORD_OK;
 }
 
-// Upload a row-major p x p matrix (host or device) into a slab buffer.
-int upload_slabs(concord_solver* s, const double* src, int32_t where, double* dst) {
-    const double* dsrc = src;
-    if (where == CONCORD_HOST) {
-        int rc = ensure_stage(s);
-        if (rc) return rc;
-        CK(cudaMemcpyAsync(s->stage, src, sizeof(double) * (size_t)s->p * s->p, cudaMemcpyHostToDevice,
-                           s->stream));
-        dsrc = s->stage;
-    }
-    CK(launch_pack_slabs(dsrc, s->p, dst, s->p, s->w, s->nblk, s->stream));
-    return CONCORD_OK;
-}
-
 int download_slabs(concord_solver* s, const double* src, double* out, int32_t where) {
     if (where == CONCORD_DEVICE) {
-        CK(launch_unpack_slabs(src, out, s->p, s->w, s->stream));
+        CK(launch_unpack_slabs(src, out, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
         CK(cudaStreamSynchronize(s->stream));
         return CONCORD_OK;
     }
     int rc = ensure_stage(s);
     if (rc) return rc;
-    CK(launch_unpack_slabs(src, s->stage, s->p, s->w, s->stream));
-    CK(cudaMemcpyAsync(out, s->stage, sizeof(double) * (size_t)s->p * s->p, cudaMemcpyDeviceToHost, s->stream));
+    CK(launch_unpack_slabs(src, s->stage, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
+    CK(cudaMemcpyAsync(out, s->stage, sizeof(double) * (size_t)s->p * ncols_local(s), cudaMemcpyDeviceToHost,
+                       s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return CONCORD_OK;
 }
 
-// Warm start: Omega slab from omega_init, W = Omega_init * T through a CSR copy.
+// Warm start: Omega slabs from omega_init, W = Omega_init * T through a CSR copy.
 int init_warm(concord_solver* s, const double* om, int32_t where) {
     const int p = s->p;
     std::vector<double> host;
@@ -217,62 +245,82 @@ int init_warm(concord_solver* s, const double* om, int32_t where) {
         CK(cudaMemcpyAsync(s->csr_col, col.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, s->stream));
         CK(cudaMemcpyAsync(s->csr_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s->stream));
     }
-    int rc = upload_slabs(s, h, CONCORD_HOST, s->Om);
+    int rc = ensure_stage(s);
     if (rc) return rc;
-    CK(launch_wform_init_csr(s->csr_rowptr, s->csr_col, s->csr_val, s->T, s->W, p, s->w, s->nblk, s->stream));
+    CK(cudaMemcpyAsync(s->stage, h, sizeof(double) * (size_t)p * p, cudaMemcpyHostToDevice, s->stream));
+    CK(launch_pack_slabs(s->stage, p, s->Om, p, s->w, s->nblk_launch, s->blk0, s->stream));
+    CK(launch_wform_init_csr(s->csr_rowptr, s->csr_col, s->csr_val, s->T, s->W, p, s->w, s->nblk_launch,
+                             s->stream));
     CK(cudaStreamSynchronize(s->stream));  // host vectors go out of scope
     return CONCORD_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int concord_abi_version(void) { return CONCORD_ABI_VERSION; }
-
-const char* concord_last_error(void) { return g_err.c_str(); }
-
-int concord_device_count(int* count) {
-    int c = 0;
-    cudaError_t e = cudaGetDeviceCount(&c);
-    if (e != cudaSuccess) c = 0;
-    if (count) *count = c;
-    return CONCORD_OK;
+WformCopies copies(const concord_solver* s) {
+    WformCopies x;
+    memset(&x, 0, sizeof(x));
+    for (int r = 0; r < s->G; ++r) {
+        char* base = static_cast<char*>(s->arena[r]);
+        x.pub[r] = reinterpret_cast<double2*>(base + s->L.pub);
+        x.dring[r] = reinterpret_cast<double*>(base + s->L.dring);
+        x.list_rs[r] = reinterpret_cast<int2*>(base + s->L.list_rs);
+        x.list_dn[r] = reinterpret_cast<double2*>(base + s->L.list_dn);
+        x.list_cnt[r] = reinterpret_cast<int*>(base + s->L.list_cnt);
+        x.bar[r] = reinterpret_cast<unsigned long long*>(base + s->L.bar);
+        x.dmax[r] = reinterpret_cast<unsigned long long*>(base + s->L.dmax);
+    }
+    return x;
 }
 
-int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_solver** out) {
+// Common constructor: G shards of nblk_loc slabs; rank < 0 keeps every shard on `device`.
+int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards, int32_t rank,
+                  concord_solver** out) {
     if (!out) return fail(CONCORD_ERR_ARG, "out is NULL");
     *out = nullptr;
     if (p < 2) return fail(CONCORD_ERR_ARG, "T must be square with p >= 2, got p=%lld", (long long)p);
     if (p > (1LL << 30)) return fail(CONCORD_ERR_ARG, "p=%lld too large", (long long)p);
+    if (n_shards < 1 || n_shards > WFORM_MAX_SHARDS)
+        return fail(CONCORD_ERR_ARG, "n_shards=%d outside [1,%d]", n_shards, WFORM_MAX_SHARDS);
+    if (rank >= n_shards) return fail(CONCORD_ERR_ARG, "rank %d >= n_shards %d", rank, n_shards);
     int rc = check_device(device);
     if (rc) return rc;
     DeviceGuard g(device);
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     const int ip = (int)p;
+    const int G = n_shards;
+    // CTAs one launch may use: all shards share the device when rank < 0
     int w;
     if (n_blocks > 0) {
         w = (ip + n_blocks - 1) / n_blocks;
     } else {
-        w = (ip + nsm - 1) / nsm;
+        const int tot = (rank < 0) ? nsm : nsm * G;
+        w = (ip + tot - 1) / tot;
         if (w < 8) w = 8;
     }
     w = (w + 1) & ~1;
-    int max_blocks = 0;
+    int nblk_loc = 0;
     for (;;) {
-        if (w > WFORM_THREADS) return fail(CONCORD_ERR_ARG, "p=%d needs slab width %d > %d", ip, w, WFORM_THREADS);
-        CK(wform_max_blocks(w, ip, &max_blocks));
-        if ((ip + w - 1) / w <= max_blocks && (ip + w - 1) / w <= WFORM_MAX_BLOCKS) break;
+        if (w > 4096) return fail(CONCORD_ERR_ARG, "p=%d needs slab width %d (too wide)", ip, w);
+        const int need = (ip + w - 1) / w;
+        nblk_loc = (need + G - 1) / G;
+        int max_blocks = 0;
+        CK(wform_max_blocks(w, ip, nblk_loc * G, &max_blocks));
+        const int launch = (rank < 0) ? nblk_loc * G : nblk_loc;
+        if (launch <= max_blocks && nblk_loc * G <= WFORM_MAX_BLOCKS) break;
         w += 2;
     }
     concord_solver* s = new concord_solver();
     s->dev = device;
     s->p = ip;
     s->w = w;
-    s->nblk = (ip + w - 1) / w;
+    s->G = G;
+    s->rank = rank;
+    s->nblk_loc = nblk_loc;
+    s->nblk_tot = nblk_loc * G;
+    s->blk0 = (rank < 0) ? 0 : rank * nblk_loc;
+    s->nblk_launch = (rank < 0) ? s->nblk_tot : nblk_loc;
     s->slab = (long long)ip * w;
-    const size_t tot = (size_t)s->nblk * s->slab;
+    const size_t tot = (size_t)s->nblk_launch * s->slab;
     auto cleanup = [&](int code) {
         concord_solver_destroy(s);
         return code;
@@ -293,31 +341,105 @@ int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_s
     CKC(cudaMemsetAsync(s->W, 0, sizeof(double) * tot, s->stream));
     CKC(cudaMemsetAsync(s->Om, 0, sizeof(double) * tot, s->stream));
     CKC(dalloc(&s->tdiag, ip));
-    CKC(dalloc(&s->pub, 3 * (size_t)ip));
+    CKC(dalloc(&s->diagd, (size_t)s->nblk_launch * ip));
     {
         const int half = (ip + (ip & 1)) / 2;
         int share_min = WFORM_SHARE_MIN;
         if (const char* e = getenv("CONCORD_SHARE_MIN")) share_min = atoi(e);
-        s->share = (half + s->nblk - 1) / s->nblk;
+        s->share = (half + s->nblk_tot - 1) / s->nblk_tot;
         if (s->share < share_min) s->share = share_min < half ? share_min : half;
         s->nsh = (half + s->share - 1) / s->share;
         s->lmax = wform_lag_cap(w, 2 * half - 1);
         s->rd = s->lmax + 3;
         s->rl = s->lmax + 4;
-        const size_t entries = (size_t)s->rl * s->nblk * s->share;
-        CKC(dalloc(&s->list_rs, entries));
-        CKC(dalloc(&s->list_dn, entries));
-        CKC(dalloc(&s->list_cnt, (size_t)s->rl * s->nblk));
-        CKC(dalloc(&s->dring, (size_t)s->rd * ip));
-        CKC(dalloc(&s->diagd, (size_t)s->nblk * ip));
+        s->L = arena_layout(ip, s->rd, s->rl, s->nblk_tot, s->share);
     }
-    CKC(dalloc(&s->bar, 1));
+    for (int r = 0; r < G; ++r) {
+        if (rank >= 0 && r != rank) continue;  // peers' arenas are opened by concord_shard_open_peers
+        CKC(cudaMalloc(&s->arena[r], s->L.bytes));
+        s->arena_owned[r] = true;
+        CKC(cudaMemsetAsync(s->arena[r], 0, s->L.bytes, s->stream));
+    }
+    s->peers_open = (rank < 0) || G == 1;
     CKC(dalloc(&s->edges, 1));
     CKC(dalloc(&s->status, 2));
     for (auto& e : s->ev) CKC(cudaEventCreate(&e));
     CKC(cudaStreamSynchronize(s->stream));
 #undef CKC
     *out = s;
+    return CONCORD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int concord_abi_version(void) { return CONCORD_ABI_VERSION; }
+
+const char* concord_last_error(void) { return g_err.c_str(); }
+
+int concord_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) c = 0;
+    if (count) *count = c;
+    return CONCORD_OK;
+}
+
+int concord_solver_create(int64_t p, int32_t device, int32_t n_blocks, concord_solver** out) {
+    return create_common(p, device, n_blocks, 1, -1, out);
+}
+
+int concord_solver_create_sharded(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
+                                  concord_solver** out) {
+    return create_common(p, device, n_blocks, n_shards, -1, out);
+}
+
+int concord_shard_create(int64_t p, int32_t n_shards, int32_t rank, int32_t device, int32_t n_blocks,
+                         concord_solver** out) {
+    if (rank < 0) return fail(CONCORD_ERR_ARG, "rank must be >= 0");
+    return create_common(p, device, n_blocks, n_shards, rank, out);
+}
+
+int concord_shard_ipc_handle(concord_solver* s, void* handle_out) {
+    if (!s || !handle_out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (s->rank < 0) return fail(CONCORD_ERR_ARG, "not a process shard");
+    DeviceGuard g(s->dev);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, s->arena[s->rank]));
+    static_assert(sizeof(cudaIpcMemHandle_t) <= CONCORD_SHARD_HANDLE_BYTES, "handle size");
+    memset(handle_out, 0, CONCORD_SHARD_HANDLE_BYTES);
+    memcpy(handle_out, &h, sizeof(h));
+    return CONCORD_OK;
+}
+
+int concord_shard_open_peers(concord_solver* s, const void* handles) {
+    if (!s || !handles) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (s->rank < 0) return fail(CONCORD_ERR_ARG, "not a process shard");
+    DeviceGuard g(s->dev);
+    const unsigned char* hb = static_cast<const unsigned char*>(handles);
+    for (int r = 0; r < s->G; ++r) {
+        if (r == s->rank || s->arena[r]) continue;
+        cudaIpcMemHandle_t h;
+        memcpy(&h, hb + (size_t)r * CONCORD_SHARD_HANDLE_BYTES, sizeof(h));
+        CK(cudaIpcOpenMemHandle(&s->arena[r], h, cudaIpcMemLazyEnablePeerAccess));
+        s->arena_owned[r] = false;
+    }
+    s->peers_open = true;
+    return CONCORD_OK;
+}
+
+int concord_solver_layout(concord_solver* s, concord_layout* out) {
+    if (!s || !out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    out->p = s->p;
+    out->slab_width = s->w;
+    out->n_shards = s->G;
+    out->rank = s->rank;
+    out->blocks_per_shard = s->nblk_loc;
+    out->blocks_total = s->nblk_tot;
+    out->col0 = s->blk0 * s->w < s->p ? s->blk0 * s->w : s->p;
+    out->ncols = ncols_local(s);
+    out->lag_cap = s->lmax;
     return CONCORD_OK;
 }
 
@@ -330,20 +452,18 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->Om);
     cudaFree(s->tdiag);
     cudaFree(s->stage);
-    cudaFree(s->pub);
-    cudaFree(s->bar);
+    cudaFree(s->diagd);
+    for (int r = 0; r < WFORM_MAX_SHARDS; ++r) {
+        if (!s->arena[r]) continue;
+        if (s->arena_owned[r]) cudaFree(s->arena[r]);
+        else cudaIpcCloseMemHandle(s->arena[r]);
+    }
     cudaFree(s->edges);
     cudaFree(s->status);
     cudaFree(s->rec_delta);
     cudaFree(s->rec_obj);
     cudaFree(s->rec_time);
     cudaFree(s->rec_nnz);
-    cudaFree(s->rec_dmax);
-    cudaFree(s->list_rs);
-    cudaFree(s->list_dn);
-    cudaFree(s->list_cnt);
-    cudaFree(s->dring);
-    cudaFree(s->diagd);
     cudaFree(s->csr_rowptr);
     cudaFree(s->csr_col);
     cudaFree(s->csr_val);
@@ -366,10 +486,8 @@ int concord_solver_set_gram(concord_solver* s, const double* T, double n, int32_
     if (!s || !T) return fail(CONCORD_ERR_ARG, "NULL argument");
     if (!(n >= 1.0)) return fail(CONCORD_ERR_ARG, "n must be at least 1");
     DeviceGuard g(s->dev);
-    int rc = upload_slabs(s, T, where, s->T);
-    if (rc) return rc;
     s->n = n;
-    return finish_gram(s);
+    return set_gram_rowmajor(s, T, where);
 }
 
 int concord_solver_gram_from_data(concord_solver* s, const double* X, int64_t n, int32_t where) {
@@ -383,13 +501,15 @@ int concord_solver_gram_from_data(concord_solver* s, const double* X, int64_t n,
         CK(cudaMemcpyAsync(tmp, X, sizeof(double) * (size_t)n * s->p, cudaMemcpyHostToDevice, s->stream));
         Xd = tmp;
     }
-    cudaError_t e = cudaMemsetAsync(s->T, 0, sizeof(double) * (size_t)s->nblk * s->slab, s->stream);
-    if (e == cudaSuccess) e = launch_gram_f64(Xd, n, s->p, s->p, s->T, 1, s->w, s->stream);
+    int rc = ensure_stage(s);
+    cudaError_t e = rc ? cudaErrorMemoryAllocation : cudaSuccess;
+    if (e == cudaSuccess) e = launch_gram_f64(Xd, n, s->p, s->p, s->stage, 0, 0, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (tmp) cudaFree(tmp);
+    if (rc) return rc;
     CK(e);
     s->n = (double)n;
-    return finish_gram(s);
+    return set_gram_rowmajor(s, s->stage, CONCORD_DEVICE);
 }
 
 int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where) {
@@ -402,30 +522,32 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
                        double* delta_trace, double* objective_trace, double* sweep_seconds) {
     if (!s || !prm) return fail(CONCORD_ERR_ARG, "NULL argument");
     if (!s->have_gram) return fail(CONCORD_ERR_ARG, "no Gram matrix set");
+    if (!s->peers_open) return fail(CONCORD_ERR_ARG, "shard peers not opened (concord_shard_open_peers)");
     if (!(prm->lam >= 0.0)) return fail(CONCORD_ERR_ARG, "lam must be nonnegative");
     if (!(prm->delta_tol > 0.0)) return fail(CONCORD_ERR_ARG, "delta_tol must be positive");
     if (prm->max_iter < 1) return fail(CONCORD_ERR_ARG, "max_outer_iterations must be at least 1");
+    const int pe = s->p + (s->p & 1);
+    if ((long long)prm->max_iter * pe >= (1LL << 31))
+        return fail(CONCORD_ERR_ARG, "max_outer_iterations * p too large (%d x %d)", prm->max_iter, pe);
     DeviceGuard g(s->dev);
     int rc = ensure_records(s, prm->max_iter);
     if (rc) return rc;
-    const size_t tot = (size_t)s->nblk * s->slab;
+    const size_t tot = (size_t)s->nblk_launch * s->slab;
 
     CK(cudaEventRecord(s->ev[0], s->stream));
     if (prm->omega_init) {
         rc = init_warm(s, prm->omega_init, prm->init_where);
         if (rc) return rc;
     } else {
-        CK(launch_slab_identity(s->Om, s->p, s->w, s->nblk, s->stream));
+        CK(launch_slab_identity(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
         CK(cudaMemcpyAsync(s->W, s->T, sizeof(double) * tot, cudaMemcpyDeviceToDevice, s->stream));
     }
-    CK(cudaMemsetAsync(s->bar, 0, sizeof(unsigned long long), s->stream));
     CK(cudaMemsetAsync(s->rec_nnz, 0, sizeof(long long) * prm->max_iter, s->stream));
-    CK(cudaMemsetAsync(s->rec_dmax, 0, sizeof(unsigned long long) * prm->max_iter, s->stream));
     CK(cudaEventRecord(s->ev[1], s->stream));
 
     WformArgs a;
+    memset(&a, 0, sizeof(a));
     a.p = s->p;
-    const int pe = s->p + (s->p & 1);
     a.m = pe - 1;
     a.half = pe / 2;
     a.w = s->w;
@@ -434,32 +556,33 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     a.T = s->T;
     a.Om = s->Om;
     a.tdiag = s->tdiag;
-    a.pub = s->pub;
+    a.diagd = s->diagd;
+    a.x = copies(s);
+    a.G = s->G;
+    a.nblk_loc = s->nblk_loc;
+    a.nblk_tot = s->nblk_tot;
+    a.blk0 = s->blk0;
+    a.sys_scope = (s->rank >= 0 && s->G > 1) ? 1 : 0;
+    a.bar_base = s->bar_base;
+    a.it_base = s->it_base;
     a.n = s->n;
     a.shrink = s->n * prm->lam;
     a.delta_tol = prm->delta_tol;
     a.max_iter = prm->max_iter;
     a.want_trace = prm->want_trace ? 1 : 0;
-    a.bar = s->bar;
+    a.lmax = s->lmax;
+    a.rd = s->rd;
+    a.rl = s->rl;
     a.rec_delta = s->rec_delta;
     a.rec_obj = s->rec_obj;
     a.rec_time = s->rec_time;
     a.rec_nnz = s->rec_nnz;
-    a.rec_dmax = s->rec_dmax;
     a.share = s->share;
     a.nsh = s->nsh;
     a.stage_ahead = 3;
     if (const char* e = getenv("CONCORD_STAGE_AHEAD")) a.stage_ahead = atoi(e);
     if (a.stage_ahead < 2) a.stage_ahead = 2;
     if (a.stage_ahead > 3) a.stage_ahead = 3;
-    a.list_rs = s->list_rs;
-    a.list_dn = s->list_dn;
-    a.list_cnt = s->list_cnt;
-    a.dring = s->dring;
-    a.diagd = s->diagd;
-    a.lmax = s->lmax;
-    a.rd = s->rd;
-    a.rl = s->rl;
     a.status = s->status;
     unsigned long long* prof = nullptr;
     const bool want_prof = getenv("CONCORD_PHASE_PROFILE") != nullptr;
@@ -468,9 +591,9 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         CK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), s->stream));
     }
     a.prof = prof;
-    CK(launch_pcd_wform(a, s->nblk, s->stream));
+    CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
     CK(cudaEventRecord(s->ev[2], s->stream));
-    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk, s->edges, s->stream));
+    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->edges, s->stream));
 
     int status[2] = {0, 0};
     unsigned long long edges = 0;
@@ -479,6 +602,11 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     CK(cudaStreamSynchronize(s->stream));
     const int iters = status[0];
     s->last_iters = iters;
+    // every shard ran the same phases: the barrier saw (phases) * nblk_tot arrivals, one per CTA
+    // per phase plus the initial publish, minus the final diagonal step's (no arrival after it)
+    const unsigned long long phases = (unsigned long long)iters * (unsigned long long)pe;
+    s->bar_base += phases * (unsigned long long)s->nblk_tot;
+    s->it_base += iters;
     std::vector<double> dl(iters > 0 ? iters : 1);
     std::vector<unsigned long long> tm(iters + 1);
     CK(cudaMemcpy(dl.data(), s->rec_delta, sizeof(double) * iters, cudaMemcpyDeviceToHost));
@@ -489,12 +617,12 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         for (int i = 0; i < iters; ++i) sweep_seconds[i] = (double)(tm[i + 1] - tm[i]) * 1e-9;
     if (objective_trace) {
         if (prm->want_trace) {
-            std::vector<double> ro((size_t)iters * s->nblk * 3);
+            std::vector<double> ro((size_t)iters * s->nblk_launch * 3);
             CK(cudaMemcpy(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost));
             for (int i = 0; i < iters; ++i) {
                 double q = 0.0, pen = 0.0, lg = 0.0;
-                for (int b = 0; b < s->nblk; ++b) {
-                    const double* r = &ro[((size_t)i * s->nblk + b) * 3];
+                for (int b = 0; b < s->nblk_launch; ++b) {
+                    const double* r = &ro[((size_t)i * s->nblk_launch + b) * 3];
                     q += r[0];
                     pen += r[1];
                     lg += r[2];
@@ -511,9 +639,9 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         cudaFree(prof);
         int clk_khz = 0;
         cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, s->dev);
-        const double phases = (double)pc[3];
-        fprintf(stderr, "[concord phase profile] p=%d iters=%d phases=%.0f lmax=%d clk=%d kHz (CTA 0)\n", s->p, iters,
-                phases, s->lmax, clk_khz);
+        const double ph = (double)pc[3];
+        fprintf(stderr, "[concord phase profile] p=%d iters=%d phases=%.0f lmax=%d shards=%d clk=%d kHz (CTA 0)\n",
+                s->p, iters, ph, s->lmax, s->G, clk_khz);
         const char* names[12] = {"chain: barrier wait", "chain: stage wait", "chain: publish+share+arrive", "-",
                                  "apply: busy", "apply: idle", "apply: batches", "chain:  publish (tc0)",
                                  "chain:  bar+fence+arrive", "chain:  share (last thread)", "apply:  heads+stage",
@@ -521,9 +649,9 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         for (int i = 0; i < 12; ++i) {
             if (i == 3 || i == 6) continue;
             const double us = pc[i] / (clk_khz * 1e-3);
-            fprintf(stderr, "  %-30s %12.1f us total  %9.3f us/phase\n", names[i], us, us / (phases > 0 ? phases : 1));
+            fprintf(stderr, "  %-30s %12.1f us total  %9.3f us/phase\n", names[i], us, us / (ph > 0 ? ph : 1));
         }
-        fprintf(stderr, "  %-30s %12llu (%.2f phases/batch)\n", names[6], pc[6], pc[6] ? phases / pc[6] : 0.0);
+        fprintf(stderr, "  %-30s %12llu (%.2f phases/batch)\n", names[6], pc[6], pc[6] ? ph / pc[6] : 0.0);
     }
     float setup_ms = 0.f, kernel_ms = 0.f;
     CK(cudaEventElapsedTime(&setup_ms, s->ev[0], s->ev[1]));
@@ -535,13 +663,34 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         res->edge_count = (int64_t)edges;
         res->kernel_ms = kernel_ms;
         res->setup_ms = setup_ms;
-        res->n_blocks = s->nblk;
+        res->n_blocks = s->nblk_tot;
         res->slab_width = s->w;
     }
     if (!status[1]) {
         fail(CONCORD_NOT_CONVERGED, "no convergence after %d outer iterations, final delta %.3e", iters,
              iters > 0 ? dl[iters - 1] : INFINITY);
         return CONCORD_NOT_CONVERGED;
+    }
+    return CONCORD_OK;
+}
+
+int concord_solver_objective_parts(concord_solver* s, double* parts, int32_t cap) {
+    if (!s || !parts) return fail(CONCORD_ERR_ARG, "NULL argument");
+    DeviceGuard g(s->dev);
+    const int k = s->last_iters < cap ? s->last_iters : cap;
+    std::vector<double> ro((size_t)k * s->nblk_launch * 3);
+    if (k > 0) CK(cudaMemcpy(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < k; ++i) {
+        double q = 0.0, pen = 0.0, lg = 0.0;
+        for (int b = 0; b < s->nblk_launch; ++b) {
+            const double* r = &ro[((size_t)i * s->nblk_launch + b) * 3];
+            q += r[0];
+            pen += r[1];
+            lg += r[2];
+        }
+        parts[3 * i] = q;
+        parts[3 * i + 1] = pen;
+        parts[3 * i + 2] = lg;
     }
     return CONCORD_OK;
 }
@@ -556,7 +705,7 @@ int concord_solver_edge_count(concord_solver* s, int64_t* out) {
     if (!s || !out) return fail(CONCORD_ERR_ARG, "NULL argument");
     DeviceGuard g(s->dev);
     unsigned long long edges = 0;
-    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk, s->edges, s->stream));
+    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->edges, s->stream));
     CK(cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     *out = (int64_t)edges;

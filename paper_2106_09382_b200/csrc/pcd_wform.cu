@@ -48,6 +48,11 @@
 
 namespace concord {
 
+// Loops over the shard copies of the exchange buffers with compile-time indices
+// (the pointer arrays stay in the kernel-parameter bank instead of a local copy).
+#define FOR_COPIES(r) _Pragma("unroll") for (int r = 0; r < WFORM_MAX_SHARDS; ++r) if (r < G)
+#define FOR_COPIES_A(r) _Pragma("unroll") for (int r = 0; r < WFORM_MAX_SHARDS; ++r) if (r < a.G)
+
 constexpr int kThreads = WFORM_THREADS;
 constexpr int kChainWarps = WFORM_CHAIN_WARPS;
 constexpr int kChain = kChainWarps * 32;
@@ -191,6 +196,15 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
     }
 }
 
+// Arrive on the grid barrier of every shard: make this CTA's exchange-buffer
+// stores visible (GPU scope, or system scope when the shards are separate
+// GPUs reached over NVLink), then bump every copy of the arrival counter.
+__device__ __forceinline__ void arrive_all(const WformArgs& a) {
+    if (a.sys_scope) __threadfence_system();
+    else __threadfence();
+    FOR_COPIES_A(r) atomicAdd(a.x.bar[r], 1ull);
+}
+
 struct Smem {
     double* stage;  // [kSlots][2 + lmax][w]: W, Om, T of the uncovered phases
     int* s_off;     // [kBatch * nblk + 1]
@@ -216,14 +230,36 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
     __shared__ int s_nent, s_multi;       // apply: single-entry segments gathered / a segment had more
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.x, nblk = gridDim.x;
+    const int bl = blockIdx.x;        // slab of this launch
+    const int b = a.blk0 + bl;        // global CTA = global column block
+    const int nblk = a.nblk_tot;
+    const int G = a.G;
+    const int shard = b / a.nblk_loc;  // whose copy of the exchange buffers is "ours"
     const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half, lmax = a.lmax;
     const int c0 = b * w;
-    const int wl = min(w, p - c0);
+    const int wl = max(0, min(w, p - c0));
     const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
-    double* __restrict__ Wb = a.W + (long long)b * a.slab;
-    const double* __restrict__ Tb = a.T + (long long)b * a.slab;
-    double* __restrict__ Ob = a.Om + (long long)b * a.slab;
+    double* __restrict__ Wb = a.W + (long long)bl * a.slab;
+    const double* __restrict__ Tb = a.T + (long long)bl * a.slab;
+    double* __restrict__ Ob = a.Om + (long long)bl * a.slab;
+    const double2* pubL = a.x.pub[0];
+    const double* dringL = a.x.dring[0];
+    const int2* lrsL = a.x.list_rs[0];
+    const double2* ldnL = a.x.list_dn[0];
+    const int* lcntL = a.x.list_cnt[0];
+    unsigned long long* barL = a.x.bar[0];
+    const unsigned long long* dmaxL = a.x.dmax[0];
+#pragma unroll
+    for (int r = 1; r < WFORM_MAX_SHARDS; ++r)
+        if (r == shard) {
+            pubL = a.x.pub[r];
+            dringL = a.x.dring[r];
+            lrsL = a.x.list_rs[r];
+            ldnL = a.x.list_dn[r];
+            lcntL = a.x.list_cnt[r];
+            barL = a.x.bar[r];
+            dmaxL = a.x.dmax[r];
+        }
     const int ssz = (2 + lmax) * w;  // doubles per stage slot
 
     Smem sm;
@@ -271,20 +307,20 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
     }
     __syncthreads();
 
-    unsigned long long* prof = (a.prof && b == 0) ? a.prof : nullptr;
+    unsigned long long* prof = (a.prof && bl == 0) ? a.prof : nullptr;
 
     if (warp < kChainWarps) {
         // ============================================================ chain warps
         const int tc = tid;
         // initial publish (phase 0, no corrections)
         for (int j = tc; j < wl; j += kChain)
-            if (pub_row(0, c0 + j, m, p) >= 0) a.pub[c0 + j] = make_double2(sm.stage[j], sm.stage[w + j]);
+            if (pub_row(0, c0 + j, m, p) >= 0) {
+                const double2 v = make_double2(sm.stage[j], sm.stage[w + j]);
+                FOR_COPIES(r) a.x.pub[r][c0 + j] = v;
+            }
         bar_chain();
-        if (tc == 0) {
-            __threadfence();
-            atomicAdd(a.bar, 1ull);
-        }
-        if (b == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
+        if (tc == 0) arrive_all(a);
+        if (bl == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
 
         int g = 0, ph = 0, it = 0, converged = 0;
         double smax = 0.0;  // max |delta| over this thread's share of the sweep
@@ -293,41 +329,45 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         while (true) {
             long long t0 = clock64();
             if (tc == 0) {
-                const unsigned long long target = (unsigned long long)(g + 1) * (unsigned long long)nblk;
-                while (ld_acquire_u64(a.bar) < target) {
+                const unsigned long long target = a.bar_base + (unsigned long long)(g + 1) * (unsigned long long)nblk;
+                while (ld_acquire_u64(barL) < target) {
                 }
                 st_vol(&s_epoch, g);
             }
             bar_chain();
             long long t1 = clock64();
             t_wait += t1 - t0;
-            const double2* __restrict__ pb = a.pub + (size_t)(g % 3) * p;
-            double2* __restrict__ pn = a.pub + (size_t)((g + 1) % 3) * p;
-            double* __restrict__ dg = a.dring + (size_t)(g % a.rd) * p;
+            const double2* __restrict__ pb = pubL + (size_t)(g % 3) * p;
+            const size_t pn_off = (size_t)((g + 1) % 3) * p;
+            const size_t dg_off = (size_t)(g % a.rd) * p;
 
             bool stop = false;
             if (ph == m) {
                 // ---- diagonal step: every CTA evaluates all p closed forms (_ckernels.pyx:41-50)
-                double2* dd = a.diagd + (size_t)b * p;
+                double2* dd = a.diagd + (size_t)bl * p;
                 double dm = 0.0;
                 for (int i = tc; i < p; i += kChain) {
                     const double2 v = ldcg2(pb + i);
                     const double nv = diag_from_dot(v.x, v.y, __ldg(a.tdiag + i), a.n);
                     const double d = __dsub_rn(nv, v.y);
                     dd[i] = make_double2(d, nv);
-                    if ((unsigned)(i - c0) < (unsigned)wl) dg[i] = d;
+                    if ((unsigned)(i - c0) < (unsigned)wl)
+                        FOR_COPIES(r) a.x.dring[r][dg_off + i] = d;
                     dm = fmax(dm, fabs(d));
                 }
                 dm = warp_max(dm);
                 if (lane == 0) s_red[0][warp] = dm;
                 bar_chain();
-                double dmax_all = __longlong_as_double((long long)__ldcg(a.rec_dmax + it));
+                double dmax_all =
+                    __longlong_as_double((long long)__ldcg(dmaxL + (a.it_base + it) % WFORM_DMAX_RING));
                 for (int j = 0; j < kChainWarps; ++j) dmax_all = fmax(dmax_all, s_red[0][j]);
                 stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter);
-                if (b == 0 && tc == 0) {
+                if (bl == 0 && tc == 0) {
                     a.rec_delta[it] = dmax_all;
                     a.rec_time[it + 1] = globaltimer_ns();
                 }
+                if (b == 0 && tc == 0)  // recycle the accumulator of sweep it+2 (last read at sweep it-2)
+                    FOR_COPIES(r) a.x.dmax[r][(a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
                 if (stop) {
                     converged = dmax_all < a.delta_tol;
                     bar_chain();
@@ -365,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
 #pragma unroll
                     for (int i = 0; i < kMaxLag; ++i) {
                         const int k = C + 1 + i;
-                        dk[i] = (i < L - 1) ? __ldcg(a.dring + (size_t)(k % a.rd) * p + x) : 0.0;
+                        dk[i] = (i < L - 1) ? __ldcg(dringL + (size_t)(k % a.rd) * p + x) : 0.0;
                     }
                     const int y = src_row(ph, x, m);
                     const double dlast = (y < p) ? row_delta(ph, x, y, pb, a.tdiag, m, a.shrink, a.n) : 0.0;
@@ -375,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     for (int i = 0; i < kMaxLag; ++i)
                         if (i < L - 1 && dk[i] != 0.0) val = fma(dk[i], st[(2 + i) * w + j], val);
                     if (dlast != 0.0) val = fma(dlast, st[(2 + L - 1) * w + j], val);
-                    pn[c] = make_double2(val, om);
+                    const double2 v = make_double2(val, om);
+                    FOR_COPIES(r) a.x.pub[r][pn_off + c] = v;
                 }
             }
 
@@ -385,8 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             const int lslot = g % a.rl;
             if (ph < m && b < a.nsh) {
                 const int c1 = m - 1 - ph;
-                int2* seg_rs = a.list_rs + ((size_t)lslot * nblk + b) * a.share;
-                double2* seg_dn = a.list_dn + ((size_t)lslot * nblk + b) * a.share;
+                const size_t seg_off = ((size_t)lslot * nblk + b) * a.share;
                 const int sid = kChain - 1 - tc;  // share work starts on the last chain warps
                 for (int base = q_lo; base < q_hi; base += kChain) {
                     const int q = base + sid;
@@ -397,14 +437,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         if (s < p) {
                             d = pair_delta(ldcg2(pb + r), ldcg2(pb + s), __ldg(a.tdiag + r), __ldg(a.tdiag + s),
                                            a.shrink, nv);
-                            dg[r] = d;
-                            dg[s] = d;
+                            FOR_COPIES(c) {
+                                a.x.dring[c][dg_off + r] = d;
+                                a.x.dring[c][dg_off + s] = d;
+                            }
                             if (d != 0.0) {
                                 smax = fmax(smax, fabs(d));
                                 ++snnz;
                             }
                         } else {
-                            dg[r] = 0.0;  // partner is the phantom (odd p)
+                            FOR_COPIES(c) a.x.dring[c][dg_off + r] = 0.0;  // phantom partner (odd p)
                         }
                     }
                     const unsigned mask = __ballot_sync(0xffffffffu, d != 0.0);
@@ -414,8 +456,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         basepos = __shfl_sync(0xffffffffu, basepos, 0);
                         if (d != 0.0) {
                             const int at = basepos + __popc(mask & ((1u << lane) - 1u));
-                            seg_rs[at] = make_int2(r, s);
-                            seg_dn[at] = make_double2(d, nv);
+                            FOR_COPIES(c) {
+                                a.x.list_rs[c][seg_off + at] = make_int2(r, s);
+                                a.x.list_dn[c][seg_off + at] = make_double2(d, nv);
+                            }
                         }
                     }
                 }
@@ -435,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             bar_chain();
             if (tc == 0) {
                 if (ph < m && b < a.nsh) {
-                    a.list_cnt[(size_t)lslot * nblk + b] = s_cnt;
+                    FOR_COPIES(r) a.x.list_cnt[r][(size_t)lslot * nblk + b] = s_cnt;
                     s_cnt = 0;
                 }
                 if (ph == m - 1 && b < a.nsh) {
@@ -444,11 +488,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         mb = fmax(mb, s_red[0][j]);
                         nbk += s_red[1][j];
                     }
-                    atomicMax(a.rec_dmax + it, (unsigned long long)__double_as_longlong(mb));
+                    FOR_COPIES(r)
+                        atomicMax(a.x.dmax[r] + (a.it_base + it) % WFORM_DMAX_RING,
+                                  (unsigned long long)__double_as_longlong(mb));
                     atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + it), (unsigned long long)nbk);
                 }
-                __threadfence();
-                atomicAdd(a.bar, 1ull);
+                arrive_all(a);
             }
             if (tc == 0) t_end += clock64() - tb;
             t_work += clock64() - t1;
@@ -517,9 +562,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             for (int idx = ta; idx < nseg; idx += kApply) {
                 const int jb = idx / nsh;
                 const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
-                const int cnt = __ldcg(a.list_cnt + seg);
-                const int2 rs = __ldcg(a.list_rs + (size_t)seg * a.share);
-                const double2 dn = __ldcg(a.list_dn + (size_t)seg * a.share);
+                const int cnt = __ldcg(lcntL + seg);
+                const int2 rs = __ldcg(lrsL + (size_t)seg * a.share);
+                const double2 dn = __ldcg(ldnL + (size_t)seg * a.share);
                 sm.s_off[idx] = cnt;
                 if (cnt > 1) s_multi = 1;
                 if (cnt == 1) {
@@ -571,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
 
             if (diag) {
                 // ---- dense diagonal step over the own slab (+ objective records)
-                const double2* dd = a.diagd + (size_t)b * p;
+                const double2* dd = a.diagd + (size_t)bl * p;
                 double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
                 for (int i0 = 0; i0 < p; i0 += kPairCap) {
                     const int iend = min(i0 + kPairCap, p);
@@ -649,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                             v2 += s_red[2][j];
                             v3 += s_red[3][j];
                         }
-                        double* ro = a.rec_obj + ((size_t)it0 * nblk + b) * 3;
+                        double* ro = a.rec_obj + ((size_t)it0 * gridDim.x + bl) * 3;
                         ro[0] = v1;
                         ro[1] = v2;
                         ro[2] = v3;
@@ -708,8 +753,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                             const int rank = e - sm.s_off[lo];
                             const size_t at =
                                 ((size_t)((k0 + jb) % a.rl) * nblk + (lo - jb * nsh)) * a.share + rank;
-                            const int2 rs = __ldcg(a.list_rs + at);
-                            const double2 dn = __ldcg(a.list_dn + at);
+                            const int2 rs = __ldcg(lrsL + at);
+                            const double2 dn = __ldcg(ldnL + at);
                             // segments with one entry had their Omega cells written above
                             if (sm.s_off[lo + 1] - sm.s_off[lo] > 1) {
                                 if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
@@ -767,16 +812,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         }
     }
     __syncthreads();
-    if (b == 0 && tid == 0) {
+    if (bl == 0 && tid == 0) {
         a.status[0] = s_iters;
         a.status[1] = s_conv;
     }
 }
 
 // --------------------------------------------------------------- layout kernels
-// Row-major p x p (leading dim ld) -> slab-major (zero padding).
+// Row-major p x p (leading dim ld) -> nblk slabs of width w starting at global
+// column block blk0 (zero padding past column p).
 __global__ void pack_slabs_kernel(const double* __restrict__ src, long long ld, double* __restrict__ dst,
-                                  int p, int w, int nblk) {
+                                  int p, int w, int nblk, int blk0) {
     const long long total = (long long)nblk * p * w;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
@@ -784,39 +830,40 @@ __global__ void pack_slabs_kernel(const double* __restrict__ src, long long ld, 
         const long long rem = e - b * p * w;
         const int i = (int)(rem / w);
         const int j = (int)(rem - (long long)i * w);
-        const long long c = b * w + j;
+        const long long c = (blk0 + b) * w + j;
         dst[e] = (c < p) ? src[(long long)i * ld + c] : 0.0;
     }
 }
 
-// Slab-major -> row-major p x p.
-__global__ void unpack_slabs_kernel(const double* __restrict__ src, double* __restrict__ dst, int p, int w) {
-    const long long total = (long long)p * p;
+// Slabs -> row-major p x ncols (ncols = columns the slabs hold, clipped to p).
+__global__ void unpack_slabs_kernel(const double* __restrict__ src, double* __restrict__ dst, int p, int w,
+                                    int ncols) {
+    const long long total = (long long)p * ncols;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(e / p);
-        const int c = (int)(e - (long long)i * p);
+        const int i = (int)(e / ncols);
+        const int c = (int)(e - (long long)i * ncols);
         const int b = c / w;
         dst[e] = src[(long long)b * p * w + (long long)i * w + (c - b * w)];
     }
 }
 
-__global__ void slab_diag_kernel(const double* __restrict__ slab, double* __restrict__ diag, int p, int w) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p; i += gridDim.x * blockDim.x) {
-        const int b = i / w;
-        diag[i] = slab[(long long)b * p * w + (long long)i * w + (i - b * w)];
-    }
+__global__ void rowmajor_diag_kernel(const double* __restrict__ src, double* __restrict__ diag, int p) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p; i += gridDim.x * blockDim.x)
+        diag[i] = src[(long long)i * p + i];
 }
 
-__global__ void slab_set_identity_kernel(double* __restrict__ slab, int p, int w) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p; i += gridDim.x * blockDim.x) {
-        const int b = i / w;
-        slab[(long long)b * p * w + (long long)i * w + (i - b * w)] = 1.0;
+__global__ void slab_set_identity_kernel(double* __restrict__ slab, int p, int w, int nblk, int blk0) {
+    const int c0 = blk0 * w;
+    const int c1 = min(p, (blk0 + nblk) * w);
+    for (int c = c0 + blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += gridDim.x * blockDim.x) {
+        const int b = c / w - blk0;
+        slab[(long long)b * p * w + (long long)c * w + (c - (b + blk0) * w)] = 1.0;
     }
 }
 
 // Count exact non-zeros of the strict upper triangle (model.py:249-253).
-__global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, int w, int nblk,
+__global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, int w, int nblk, int blk0,
                                        unsigned long long* __restrict__ out) {
     unsigned long long local = 0;
     const long long total = (long long)nblk * p * w;
@@ -825,7 +872,7 @@ __global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, i
         const long long b = e / ((long long)p * w);
         const long long rem = e - b * p * w;
         const int i = (int)(rem / w);
-        const long long c = b * w + (rem - (long long)i * w);
+        const long long c = (blk0 + b) * w + (rem - (long long)i * w);
         if (c < p && i < c && slab[e] != 0.0) ++local;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -875,7 +922,7 @@ size_t wform_smem_bytes(int w, int p, int nblk, int lmax) {
 }
 
 cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st) {
-    const size_t smem = wform_smem_bytes(args.w, args.p, nblk, args.lmax);
+    const size_t smem = wform_smem_bytes(args.w, args.p, args.nblk_tot, args.lmax);
     cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -884,9 +931,12 @@ cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st) {
     return cudaLaunchCooperativeKernel((void*)pcd_wform_kernel, dim3(nblk), dim3(kThreads), kargs, smem, st);
 }
 
-cudaError_t wform_max_blocks(int w, int p, int* max_blocks) {
-    const int nblk = (p + w - 1) / w;
-    const size_t smem = wform_smem_bytes(w, p, nblk, wform_lag_cap(w, p + (p & 1) - 1));
+cudaError_t wform_max_blocks(int w, int p, int nblk_tot, int* max_blocks) {
+    const size_t smem = wform_smem_bytes(w, p, nblk_tot, wform_lag_cap(w, p + (p & 1) - 1));
+    if (smem > 227 * 1024) {
+        *max_blocks = 0;
+        return cudaSuccess;
+    }
     cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -907,34 +957,35 @@ static int grid_for(long long total) {
     return (int)g;
 }
 
-cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk,
+cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk, int blk0,
                               cudaStream_t st) {
-    pack_slabs_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(src, ld, dst, p, w, nblk);
+    pack_slabs_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(src, ld, dst, p, w, nblk, blk0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, cudaStream_t st) {
-    unpack_slabs_kernel<<<grid_for((long long)p * p), 256, 0, st>>>(src, dst, p, w);
+cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, int nblk, int blk0, cudaStream_t st) {
+    const int ncols = max(0, min(p, (blk0 + nblk) * w) - blk0 * w);
+    unpack_slabs_kernel<<<grid_for((long long)p * ncols), 256, 0, st>>>(src, dst, p, w, ncols);
     return cudaGetLastError();
 }
 
-cudaError_t launch_slab_diag(const double* slab, double* diag, int p, int w, cudaStream_t st) {
-    slab_diag_kernel<<<grid_for(p), 256, 0, st>>>(slab, diag, p, w);
+cudaError_t launch_rowmajor_diag(const double* src, double* diag, int p, cudaStream_t st) {
+    rowmajor_diag_kernel<<<grid_for(p), 256, 0, st>>>(src, diag, p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, cudaStream_t st) {
+cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, int blk0, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(slab, 0, sizeof(double) * (size_t)nblk * p * w, st);
     if (e != cudaSuccess) return e;
-    slab_set_identity_kernel<<<grid_for(p), 256, 0, st>>>(slab, p, w);
+    slab_set_identity_kernel<<<grid_for((long long)nblk * w), 256, 0, st>>>(slab, p, w, nblk, blk0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, unsigned long long* out,
+cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, int blk0, unsigned long long* out,
                                    cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    slab_edge_count_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(slab, p, w, nblk, out);
+    slab_edge_count_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(slab, p, w, nblk, blk0, out);
     return cudaGetLastError();
 }
 

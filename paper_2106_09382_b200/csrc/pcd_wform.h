@@ -3,16 +3,44 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef WFORM_THREADS
 #define WFORM_THREADS 512
+#endif
+#ifndef WFORM_CHAIN_WARPS
 #define WFORM_CHAIN_WARPS 4     // warps 0..3: publish / closed forms / grid barrier (the colour chain)
+#endif
+#ifndef WFORM_PAIR_CAP
 #define WFORM_PAIR_CAP 1024     // delta-list pairs staged in shared memory per apply chunk
+#endif
+#ifndef WFORM_SHARE_MIN
 #define WFORM_SHARE_MIN 1       // closed forms per share CTA per colour (fewer, longer delta-list segments)
+#endif
+#ifndef WFORM_BATCH
 #define WFORM_BATCH 8           // colour phases one apply batch may cover
+#endif
+#ifndef WFORM_STAGE_SLOTS
 #define WFORM_STAGE_SLOTS 5     // publish stages in flight (shared memory ring)
+#endif
+#ifndef WFORM_MAX_LAG
 #define WFORM_MAX_LAG 8         // max phases the apply warps may trail the chain
+#endif
 #define WFORM_MAX_BLOCKS 1024
+#define WFORM_MAX_SHARDS 8       // copies of the exchange buffers (GPUs, or virtual shards on one GPU)
+#define WFORM_DMAX_RING 4        // per-sweep max |delta| accumulators (ring over sweeps)
 
 namespace concord {
+
+// Exchange buffers.  Every shard holds a full copy; writers store into all
+// copies (local HBM, or a peer GPU's HBM over NVLink), readers read their own.
+struct WformCopies {
+    double2* pub[WFORM_MAX_SHARDS];             // [3][p] published (W[x,c], Om[x,c]) per phase mod 3
+    double* dring[WFORM_MAX_SHARDS];            // [rd][p] per-row delta of each recent phase
+    int2* list_rs[WFORM_MAX_SHARDS];            // [rl][nblk_tot][share] non-zero pairs of a colour
+    double2* list_dn[WFORM_MAX_SHARDS];         // [rl][nblk_tot][share] (delta, new value)
+    int* list_cnt[WFORM_MAX_SHARDS];            // [rl][nblk_tot] segment lengths
+    unsigned long long* bar[WFORM_MAX_SHARDS];  // grid-barrier arrival counter (all CTAs of all shards)
+    unsigned long long* dmax[WFORM_MAX_SHARDS]; // [WFORM_DMAX_RING] per-sweep max |off-diagonal delta| bits
+};
 
 struct WformArgs {
     int p;          // problem size
@@ -24,9 +52,15 @@ struct WformArgs {
     const double* T;
     double* Om;     // slab-major dense Omega
     const double* tdiag;
-    double2* pub;   // 3 * p rotating publish buffers (global phase mod 3)
-    double* dring;  // [rd][p] per-row delta of each recent phase (0.0 where the pair did not move)
-    double2* diagd; // [nblk][p] (delta, new) of the last diagonal step, per CTA
+    double2* diagd; // [launch CTAs][p] (delta, new) of the last diagonal step, per CTA
+    WformCopies x;  // exchange buffers, one copy per shard
+    int G;          // shards
+    int nblk_loc;   // CTAs (column slabs) per shard
+    int nblk_tot;   // CTAs over all shards
+    int blk0;       // global index of this launch's first CTA (its first slab)
+    int sys_scope;  // 1: shards are separate GPUs (system-scope fences for peer stores)
+    unsigned long long bar_base;  // arrival count of the barrier at the start of this fit (same on all shards)
+    int it_base;                  // sweeps run by earlier fits (indexes the dmax ring)
     double n;       // sample count (GramMatrix.n)
     double shrink;  // n * lam (solver.py:285)
     double delta_tol;
@@ -35,18 +69,13 @@ struct WformArgs {
     int lmax;       // lag cap of the apply warps behind the chain (<= WFORM_MAX_LAG, <= m)
     int rd;         // dring slots (>= lmax + 3)
     int rl;         // delta-list ring slots (>= lmax + 4)
-    unsigned long long* bar;
     double* rec_delta;              // [max_iter]
     double* rec_obj;                // [max_iter][nblk][3]: <W,Om> part, sum_{i<j}|om|, sum log om_ii
     unsigned long long* rec_time;   // [max_iter + 1] globaltimer ns
-    long long* rec_nnz;             // [max_iter] non-zero off-diagonal deltas per sweep (zeroed by host)
-    unsigned long long* rec_dmax;   // [max_iter] max |off-diagonal delta| per sweep, double bits (zeroed)
+    long long* rec_nnz;             // [max_iter] non-zero off-diagonal deltas per sweep, this launch (zeroed)
     int share;                      // pairs per share CTA per colour
     int nsh;                        // CTAs that evaluate closed forms (ceil(half / share))
     int stage_ahead;                // publishes staged beyond the chain's phase
-    int2* list_rs;                  // [rl][nblk][share] non-zero pairs of a colour, per CTA segment
-    double2* list_dn;               // [rl][nblk][share] (delta, new value)
-    int* list_cnt;                  // [rl][nblk] segment lengths
     int* status;                    // [0] iterations, [1] converged
     unsigned long long* prof;       // optional [16] cycle counters (CTA 0), or NULL
 };
@@ -56,16 +85,20 @@ int wform_lag_cap(int w, int m);
 size_t wform_smem_bytes(int w, int p, int nblk, int lmax);
 
 cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st);
-cudaError_t wform_max_blocks(int w, int p, int* max_blocks);
-cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk,
+cudaError_t wform_max_blocks(int w, int p, int nblk_tot, int* max_blocks);
+// Slab-layout helpers.  `nblk` slabs of width w starting at global column block
+// blk0 (columns [blk0*w, (blk0+nblk)*w) clipped to p).
+cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk, int blk0,
                               cudaStream_t st);
-cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, cudaStream_t st);
-cudaError_t launch_slab_diag(const double* slab, double* diag, int p, int w, cudaStream_t st);
-cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, cudaStream_t st);
-cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, unsigned long long* out,
+// Slabs -> row-major p x ncols block (ld = ncols) of the columns the slabs hold.
+cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, int nblk, int blk0, cudaStream_t st);
+cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, int blk0, cudaStream_t st);
+cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, int blk0, unsigned long long* out,
                                    cudaStream_t st);
 cudaError_t launch_wform_init_csr(const int* rowptr, const int* colidx, const double* vals, const double* Tslab,
                                   double* Wslab, int p, int w, int nblk, cudaStream_t st);
+// Diagonal of a row-major p x p matrix (the replicated T diagonal).
+cudaError_t launch_rowmajor_diag(const double* src, double* diag, int p, cudaStream_t st);
 
 // Exact (direct-form) reference-protocol sweeps, pcd_exact.cu.
 cudaError_t launch_pcd_sweep_exact(double* om, const double* t, int p, double n, double shrink,

@@ -155,11 +155,17 @@ class Solver:
     transient one.
     """
 
-    def __init__(self, p, device=0, n_blocks=0):
+    def __init__(self, p, device=0, n_blocks=0, n_shards=1):
         L = _lib.load()
         _lib.require_device()
         h = ctypes.c_void_p()
-        _lib.check(L.concord_solver_create(int(p), int(device), int(n_blocks), ctypes.byref(h)))
+        if n_shards == 1:
+            _lib.check(L.concord_solver_create(int(p), int(device), int(n_blocks), ctypes.byref(h)))
+        else:
+            # columns split over n_shards virtual shards with replicated exchange
+            # buffers: the multi-GPU data flow (dist.py) on one device
+            _lib.check(L.concord_solver_create_sharded(int(p), int(device), int(n_blocks), int(n_shards),
+                                                       ctypes.byref(h)))
         self._h = h
         self.p = int(p)
         self.device = int(device)
@@ -182,6 +188,12 @@ class Solver:
 
     def __exit__(self, *exc):
         self.close()
+
+    def layout(self):
+        """Column partition: slab width, shards, CTAs, this solver's column range."""
+        lay = _lib.Layout()
+        _lib.check(_lib.load().concord_solver_layout(self._h, ctypes.byref(lay)))
+        return {f: getattr(lay, f) for f, _ in _lib.Layout._fields_ if f != "reserved"}
 
     def set_stream(self, stream_ptr):
         _lib.check(_lib.load().concord_solver_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))

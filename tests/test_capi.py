@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     L = _lib.load()
     for name in _declared():
         assert hasattr(L, name), name
-    assert L.concord_abi_version() == 1
+    assert L.concord_abi_version() == _lib.ABI_VERSION
 
 
 def test_no_device_is_reported_not_hidden():

@@ -231,3 +231,43 @@ def test_objective_monotone_large_p():
     assert all(b <= a + 1e-9 * abs(a) for a, b in zip(tr, tr[1:]))
     om = rep.estimate.omega
     assert np.array_equal(om, om.T) and np.all(np.diag(om) > 0)
+
+
+# ------------------------------------------------- multi-GPU data path (8e)
+
+
+@pytest.mark.parametrize("name", ["ar2_p100_n50_l0.1", "sf_p101_n50_l0.3", "ar2_p9_n70_l0.1"])
+def test_virtual_shards_are_bitwise_invariant(golden, name):
+    """Columns split over G shards with replicated exchange buffers (the NVLink
+    data flow of dist.py, on one device): bitwise identical for G = 1, 2, 4, 8."""
+    c = case(golden, name)
+    outs = []
+    for g in (1, 2, 4, 8):
+        with cb.Solver(c["p"], n_shards=g) as s:
+            assert s.layout()["n_shards"] == g
+            s.set_gram(cb.GramMatrix(c["t"], c["n"]))
+            outs.append(s.fit(c["lam"], c["tol"], 5000))
+    for r in outs:
+        assert r.iterations == c["iters"]
+        assert np.array_equal(r.estimate.omega, outs[0].estimate.omega)
+        np.testing.assert_allclose(r.objective_trace, outs[0].objective_trace, rtol=1e-12)
+    assert_close_support(outs[0].estimate.omega, c["omega"])
+
+
+def test_virtual_shards_consecutive_fits_and_large_p(oracle):
+    """Barrier/sweep bases carried across fits; a p=2000 sweep split 8 ways."""
+    _, t = synth.problem("ar2", 2000, 1000, seed=4)
+    g = cb.GramMatrix(t, 1000)
+    with cb.Solver(2000) as s1, cb.Solver(2000, n_shards=8) as s8:
+        s1.set_gram(g)
+        s8.set_gram(g)
+        for lam in (0.5, 0.3, 0.25):
+            a = s1.fit(lam, 1e-5, 500)
+            b = s8.fit(lam, 1e-5, 500)
+            assert a.iterations == b.iterations
+            assert np.array_equal(a.estimate.omega, b.estimate.omega)
+    om = np.eye(2000)
+    rs, ss, off = oracle.circle_flat(2000)
+    ref = oracle.pcd_fit(t, 1000, 0.25, 1e-5, 500, workers=8, trace=False)
+    assert ref["iterations"] == b.iterations
+    assert_close_support(b.estimate.omega, ref["omega"])
