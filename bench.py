@@ -1,6 +1,6 @@
 """Benchmark: CONCORD-PCD on B200 vs the reference CPU path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode path|sharded]
 
 Workload (BASELINE.json configs[2], the paper workload): AR(2) truth,
 p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
@@ -18,6 +18,15 @@ lambda reported beside it.
 * cpu_baseline / --impl reference: the reference's own compiled sweep
   (oracle/_ref, built from /root/reference's _ckernels.pyx) on all host cores,
   timed on a bounded sample of rounds (sweep cost is data-independent).
+
+Multi-GPU (torchrun, one rank per GPU):
+* --mode path (default): the lambda path is split over the ranks, each GPU
+  fits its own lambdas (independent problems, no data-path collective;
+  scaling "weak").
+* --mode sharded: BASELINE configs[3] -- p=20000, n=5000 -- ONE problem
+  column-sharded over all ranks (paper_2106_09382_b200.dist): every colour's
+  published values are all-gathered in-kernel through NVLink peer stores
+  (scaling "strong"; sweeps/s of the one problem).
 """
 
 import argparse
@@ -45,13 +54,19 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--p", type=int, default=5000)
-    ap.add_argument("--n", type=int, default=2000)
+    ap.add_argument("--mode", choices=["path", "sharded"], default="path")
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--delta-tol", type=float, default=1e-5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.p is None:
+        a.p = 20000 if a.mode == "sharded" else 5000
+    if a.n is None:
+        a.n = 5000 if a.mode == "sharded" else 2000
+    return a
 
 
 # --------------------------------------------------------------- plumbing
@@ -64,12 +79,20 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
 
-    def init(self, backend="nccl"):
-        if self.world > 1:
+    def init(self, backend="nccl", force=False):
+        if self.world > 1 or force:
+            import socket
+
             import torch.distributed as dist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend)
+            if "MASTER_PORT" not in os.environ:
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            dist.init_process_group(backend, rank=self.rank, world_size=self.world,
+                                    device_id=None if backend != "nccl" else __import__("torch").device(
+                                        "cuda", self.local))
             self.pg = dist
 
     def barrier(self):
@@ -167,6 +190,8 @@ def ncu_traffic(workload):
 def make_problem(p, n):
     from paper_2106_09382_b200 import synth
 
+    if p > 8000:  # configs[3:]: banded sampler (same distribution, O(p n))
+        return synth.center(synth.sample_mvn_ar2_banded(p, n, seed=0))
     return synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
 
 
@@ -203,7 +228,8 @@ def cpu_reference_rate(t, n, lam, target_s, workers):
             orc.pcd_sweep(om, t, n, n * lam, rs, ss, sub, workers)
         return time.perf_counter() - tic
 
-    probe = max(2, min(nrounds, 8))
+    probe = max(2, min(nrounds, 32))
+    run(0, probe)  # warm (first touch of T, thread pool start)
     dt = run(0, probe)
     rounds = int(max(probe, min(nrounds, target_s / max(dt / probe, 1e-9))))
     el = run(0, rounds)
@@ -347,6 +373,63 @@ def run_e2e(args, d, s, stream, lam_at):
             "path": "paper_2106_09382_b200.pcd_fit(GramMatrix(pinned T), SolverConfig(lam)) -> FitReport"}
 
 
+def run_sharded(args, d):
+    """One p=20000 problem column-sharded over all ranks; value = sweeps/s of that problem."""
+    import torch
+
+    import paper_2106_09382_b200 as cb
+    from paper_2106_09382_b200 import dist as cdist
+
+    torch.cuda.set_device(d.local)
+    p, n, K, W = args.p, args.n, args.steps, args.warmup
+    x = make_problem(p, n)
+    g0 = time.perf_counter()
+    s = cdist.ShardedSolver(p, device=d.local)
+    s.gram_from_data(cb.DataMatrix(x, centered=True))
+    gram_s = time.perf_counter() - g0
+    lams = LAMS[:6]  # 0.55 .. 0.30: the sparse end of the path at this size
+
+    def one_fit(lam):
+        rep = s.fit(lam, args.delta_tol, 5000, trace=True, gather=False, raise_on_cap=False)
+        return rep, float(s.last_result.kernel_ms)
+
+    for i in range(W):
+        one_fit(lams[i % len(lams)])
+    clocks = Clocks(d.local)
+    d.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    fits, kern = [], 0.0
+    for i in range(K):
+        lam = lams[i % len(lams)]
+        rep, ms = one_fit(lam)
+        fits.append((lam, rep.iterations, ms, rep.edge_count))
+        kern += ms
+    torch.cuda.synchronize()
+    d.barrier()
+    clk = clocks.stop()
+    elapsed_ms = d.max(kern)  # device time of the fits (CUDA events around each kernel), max over ranks
+    sweeps = sum(f[1] for f in fits)  # one problem: every rank ran the same sweeps
+    out = {
+        "metric": f"sweeps/s (CONCORD-PCD fits, p={p} n={n}, column-sharded over {d.world} GPU(s))",
+        "value": sweeps / (elapsed_ms / 1e3), "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
+        "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic: AR(2) truth, X ~ N(0, inv(truth)) n={n} seed 0 (banded sampler), centred",
+        "config": {"workload": f"ar2 p={p} n={n} sharded", "source": "BASELINE.json configs[3]", "p": p, "n": n,
+                   "lambdas": [f[0] for f in fits], "parallelism": f"column-sharded dp{d.world} (in-kernel NVLink exchange)",
+                   "slab_width": s.slab_width, "blocks_total": s.blocks_total,
+                   "l2": "inputs larger than L2 (T, W, Omega %.1f GB)" % (24 * p * p / 1e9)},
+        "seconds_to_converge": {f"{f[0]:.2f}": round(f[2] / 1e3, 6) for f in fits},
+        "iterations": {f"{f[0]:.2f}": f[1] for f in fits},
+        "edges": {f"{f[0]:.2f}": f[3] for f in fits},
+        "gram_s_incl_h2d": round(gram_s, 3),
+        "gpu_launches": 3 * K,
+        "clocks": clk,
+    }
+    s.close()
+    return out
+
+
 # --------------------------------------------------------------- reference arm
 
 
@@ -356,7 +439,10 @@ def run_reference(args, d):
     from paper_2106_09382_b200 import synth
 
     p, n, K, W = args.p, args.n, args.steps, args.warmup
-    t = synth.host_gram(make_problem(p, n))
+    p_run = p
+    if args.mode == "sharded":  # the reference's O(p^2) schedule does not fit at p=20000: time p=5000, scale by p^3
+        p_run, n = 5000, 2000
+    t = synth.host_gram(make_problem(p_run, n))
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     per_step = max(1.0, min(args.cpu_seconds, 150.0 / max(K + W, 1)))
     rates = []
@@ -367,17 +453,24 @@ def run_reference(args, d):
         if i >= W:
             rates.append((rate, rounds, el))
         info = (rounds, el)
-    total_sweeps = sum(r[1] / (p + (p % 2) - 1) for r in rates)
+    m_run = p_run + (p_run % 2) - 1
+    total_sweeps = sum(r[1] / m_run for r in rates)
     total_s = sum(r[2] for r in rates)
     value = total_sweeps / total_s
-    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
-            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+    sample = (f"each step = {info[0]} colour rounds of the reference pcd_sweep at p={p_run} "
+              f"(compiled _ckernels, workers={os.cpu_count()}); sweeps = rounds/{m_run}")
+    if p_run != p:
+        value *= (p_run / p) ** 3  # the sweep is 16 p^3 bytes of dense dots (_ckernels.pyx:33-36)
+        sample += f"; extrapolated to p={p} by (p/{p_run})^3"
+    metric = METRIC if args.mode == "path" else f"sweeps/s (CONCORD-PCD fits, p={p} n={args.n}, column-sharded over {d.world} GPU(s))"
+    workload = f"ar2 p={p} n={args.n} lambda-path cold" if args.mode == "path" else f"ar2 p={p} n={args.n} sharded"
+    return {"metric": metric, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True,
+            "scaling": "weak" if args.mode == "path" else "strong", "vs_baseline": None,
             "dtype": "f64", "impl": "reference",
-            "data": "synthetic: AR(2) truth, X ~ N(0, inv(truth)) n=2000 seed 0, centred",
-            "config": {"workload": f"ar2 p={p} n={n} lambda-path cold", "p": p, "n": n},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
-                             "sample": f"each step = {info[0]} colour rounds of the reference pcd_sweep "
-                                       f"(compiled _ckernels, workers={os.cpu_count()}); sweeps = rounds/{p - 1 + p % 2}"},
+            "data": f"synthetic: AR(2) truth, X ~ N(0, inv(truth)) n={n} seed 0, centred",
+            "config": {"workload": workload, "p": p, "n": args.n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
 
@@ -390,9 +483,9 @@ def main():
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    d.init("nccl")
+    d.init("nccl", force=args.mode == "sharded")
     try:
-        out = run_ours(args, d)
+        out = run_sharded(args, d) if args.mode == "sharded" else run_ours(args, d)
     finally:
         d.close()
     if d.rank == 0:

@@ -79,6 +79,33 @@ def sample_mvn(omega_true, n, seed=0):
     return np.ascontiguousarray(x)
 
 
+def sample_mvn_ar2_banded(p, n, seed=0):
+    """N(0, inv(ar2_precision(p))) samples in O(p*n) for large p (configs[3:], p >= 20000).
+
+    Same distribution as sample_mvn(ar2_precision(p), n, seed) -- the same
+    normal draws z and the same triangular system L^T x = z with L the
+    (banded) Cholesky factor -- but solved with banded LAPACK routines, so the
+    last bits differ from the dense path.  Used where the dense Cholesky of a
+    p x p truth is the bottleneck and no CPU oracle exists.
+    """
+    from scipy.linalg import cholesky_banded, solve_banded
+
+    ab = np.zeros((3, p))  # lower banded storage of the AR(2) truth
+    ab[0] = 1.0
+    ab[1, :-1] = 0.45
+    ab[2, :-2] = 0.40
+    lb = cholesky_banded(ab, lower=True)  # L in lower banded storage
+    # L^T is upper triangular with 2 super-diagonals: upper banded storage u[2 + i - j, j] = L^T[i, j]
+    ub = np.zeros((3, p))
+    ub[2] = lb[0]
+    ub[1, 1:] = lb[1, :-1]
+    ub[0, 2:] = lb[2, :-2]
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((n, p))
+    x = solve_banded((0, 2), ub, z.T).T
+    return np.ascontiguousarray(x)
+
+
 def center(x):
     """model.py:182-187 (center_columns on a raw array)."""
     return x - x.mean(axis=0)

@@ -78,3 +78,14 @@ def test_cyclic_max_reduce_and_diff_vector():
     a = cb.PrecisionEstimate(np.eye(4) * 2)
     b = cb.PrecisionEstimate(np.eye(4))
     assert cb.diff_vector(a, b).shape == (10,)
+
+
+def test_banded_ar2_sampler_matches_dense_sampler():
+    """synth.sample_mvn_ar2_banded (configs[3:], large p) draws the same samples as
+    the reference sampler (datagen.py:135-154) up to rounding."""
+    from paper_2106_09382_b200 import synth
+
+    for p, n, seed in ((50, 30, 0), (301, 120, 7)):
+        a = synth.sample_mvn(synth.ar2_precision(p), n, seed=seed)
+        b = synth.sample_mvn_ar2_banded(p, n, seed=seed)
+        np.testing.assert_allclose(b, a, rtol=0, atol=1e-12 * np.abs(a).max())
