@@ -129,6 +129,15 @@ int concord_solver_get_omega(concord_solver* s, double* omega_out, int32_t where
  * (a shard's partials add up across shards). */
 int concord_solver_objective_parts(concord_solver* s, double* parts, int32_t cap);
 int concord_solver_edge_count(concord_solver* s, int64_t* out);
+/* check_optimality (model.py:256-289) of the last fit on the device, with
+ * M = Omega*T taken from the maintained W: worst stationarity violation and
+ * its coordinate (row <= col, 0-based; first in row-major order on ties). */
+int concord_solver_check_optimality(concord_solver* s, double lam, double* worst, int64_t* row, int64_t* col);
+/* The entries write_estimate (fileio.py:87-95) stores -- every diagonal and
+ * every exact non-zero with i < j -- compacted on the device in (i, j)
+ * order, 0-based.  NULL ii/jj/vv: only *count is set (size query). */
+int concord_solver_estimate_entries(concord_solver* s, int64_t* count, int32_t* ii, int32_t* jj, double* vv,
+                                    int64_t cap);
 /* Non-zero off-diagonal deltas of each sweep of the last fit (the row streams
  * the kernel applied; used for the roofline's algorithmic bytes).  Copies
  * min(cap, iterations) entries, *count = iterations of the last fit. */

@@ -31,6 +31,7 @@ EXPORTS = (
     "concord_pcd_sweep_exact", "concord_u2_sweep_exact", "concord_cd_sweep_exact",
     "concord_solver_create_sharded", "concord_solver_layout", "concord_shard_create",
     "concord_shard_ipc_handle", "concord_shard_open_peers", "concord_solver_objective_parts",
+    "concord_solver_check_optimality", "concord_solver_estimate_entries",
 )
 
 ABI_VERSION = 2
@@ -134,6 +135,9 @@ def load(build_if_missing=True):
             "concord_shard_ipc_handle": ([vp, vp], ctypes.c_int),
             "concord_shard_open_peers": ([vp, vp], ctypes.c_int),
             "concord_solver_objective_parts": ([vp, vp, i32], ctypes.c_int),
+            "concord_solver_check_optimality": ([vp, d, ctypes.POINTER(d), ctypes.POINTER(i64), ctypes.POINTER(i64)],
+                                                ctypes.c_int),
+            "concord_solver_estimate_entries": ([vp, ctypes.POINTER(i64), vp, vp, vp, i64], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

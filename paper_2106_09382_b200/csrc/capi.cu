@@ -721,6 +721,78 @@ int concord_solver_sweep_stats(concord_solver* s, int64_t* nnz_pairs, int32_t ca
     return CONCORD_OK;
 }
 
+int concord_solver_check_optimality(concord_solver* s, double lam, double* worst, int64_t* row, int64_t* col) {
+    if (!s || !worst || !row || !col) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (s->rank >= 0 && s->G > 1) return fail(CONCORD_ERR_ARG, "check_optimality needs every column on this device");
+    if (!s->have_gram || s->last_iters < 1) return fail(CONCORD_ERR_ARG, "no fitted estimate");
+    DeviceGuard g(s->dev);
+    const int nb = 148 * 4;
+    double* bv = nullptr;
+    long long* bi = nullptr;
+    CK(dalloc(&bv, nb));
+    cudaError_t e = dalloc(&bi, nb);
+    std::vector<double> hv(nb);
+    std::vector<long long> hi(nb);
+    if (e == cudaSuccess) e = launch_optimality(s->W, s->Om, s->p, s->w, s->n, s->n * lam, bv, bi, nb, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hv.data(), bv, sizeof(double) * nb, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hi.data(), bi, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(bv);
+    cudaFree(bi);
+    CK(e);
+    double best = -1.0;
+    long long bidx = 0;
+    for (int k = 0; k < nb; ++k)
+        if (hv[k] > best || (hv[k] == best && hi[k] < bidx)) {
+            best = hv[k];
+            bidx = hi[k];
+        }
+    *worst = best;
+    *row = bidx / s->p;
+    *col = bidx % s->p;
+    return CONCORD_OK;
+}
+
+int concord_solver_estimate_entries(concord_solver* s, int64_t* count, int32_t* ii, int32_t* jj, double* vv,
+                                    int64_t cap) {
+    if (!s || !count) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (s->rank >= 0 && s->G > 1) return fail(CONCORD_ERR_ARG, "estimate_entries needs every column on this device");
+    DeviceGuard g(s->dev);
+    const int p = s->p;
+    int* rowcnt = nullptr;
+    CK(dalloc(&rowcnt, p));
+    std::vector<int> hc(p);
+    cudaError_t e = launch_triplet_count(s->Om, p, s->w, rowcnt, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), rowcnt, sizeof(int) * p, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(rowcnt);
+    CK(e);
+    std::vector<long long> off(p + 1, 0);
+    for (int i = 0; i < p; ++i) off[i + 1] = off[i] + hc[i];
+    *count = off[p];
+    if (!ii || !jj || !vv) return CONCORD_OK;  // size query
+    if (cap < off[p]) return fail(CONCORD_ERR_ARG, "capacity %lld < %lld entries", (long long)cap, off[p]);
+    long long* doff = nullptr;
+    int *di = nullptr, *dj = nullptr;
+    double* dv = nullptr;
+    e = dalloc(&doff, p + 1);
+    if (e == cudaSuccess) e = dalloc(&di, off[p]);
+    if (e == cudaSuccess) e = dalloc(&dj, off[p]);
+    if (e == cudaSuccess) e = dalloc(&dv, off[p]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(doff, off.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = launch_triplet_write(s->Om, p, s->w, doff, di, dj, dv, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ii, di, sizeof(int) * off[p], cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(jj, dj, sizeof(int) * off[p], cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(vv, dv, sizeof(double) * off[p], cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    cudaFree(doff);
+    cudaFree(di);
+    cudaFree(dj);
+    cudaFree(dv);
+    CK(e);
+    return CONCORD_OK;
+}
+
 int concord_host_alloc(int64_t bytes, void** out) {
     if (!out || bytes < 0) return fail(CONCORD_ERR_ARG, "bad arguments");
     *out = nullptr;

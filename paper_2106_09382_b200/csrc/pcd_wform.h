@@ -108,6 +108,13 @@ cudaError_t launch_u2_sweep_exact(double* om, const double* t, int p, double n, 
                                   const long long* rs, const long long* ss, long long npairs, cudaStream_t st);
 cudaError_t launch_cd_sweep_exact(double* om, const double* t, int p, double n, double shrink, cudaStream_t st);
 
+// Diagnostics on the slab-resident estimate, diag.cu.
+cudaError_t launch_optimality(const double* W, const double* Om, int p, int w, double n, double weight,
+                              double* blk_val, long long* blk_idx, int nblocks, cudaStream_t st);
+cudaError_t launch_triplet_count(const double* Om, int p, int w, int* rowcnt, cudaStream_t st);
+cudaError_t launch_triplet_write(const double* Om, int p, int w, const long long* rowoff, int* ti, int* tj,
+                                 double* tv, cudaStream_t st);
+
 // FP64 DMMA Gram / GEMM, gram.cu.  T = X^T X (X: n x p row-major, leading dim ldx).
 // out_mode 0: row-major p x p (ld = p); 1: slab-major with width w.
 cudaError_t launch_gram_f64(const double* X, long long n, int p, long long ldx, double* out, int out_mode, int w,

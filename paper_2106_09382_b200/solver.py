@@ -254,6 +254,28 @@ class Solver:
         _lib.check(_lib.load().concord_solver_get_omega(self._h, _lib.ptr(out), _lib.HOST))
         return out
 
+    def check_optimality(self, lam, eps=1e-6):
+        """check_optimality (model.py:256-289) of the last fit, on the device (M = W)."""
+        from .model import OptimalityReport
+
+        worst, i, j = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.load().concord_solver_check_optimality(self._h, float(lam), ctypes.byref(worst),
+                                                               ctypes.byref(i), ctypes.byref(j)))
+        return OptimalityReport(worst_violation=worst.value, worst_coordinate=(i.value, j.value), eps=eps,
+                                ok=worst.value <= eps)
+
+    def estimate_entries(self):
+        """(i, j, value) arrays, 0-based, of every diagonal and every exact non-zero i < j,
+        in (i, j) order -- what fileio.write_estimate stores (fileio.py:87-95)."""
+        L = _lib.load()
+        cnt = ctypes.c_int64()
+        _lib.check(L.concord_solver_estimate_entries(self._h, ctypes.byref(cnt), None, None, None, 0))
+        k = cnt.value
+        ii, jj, vv = np.empty(k, np.int32), np.empty(k, np.int32), np.empty(k)
+        _lib.check(L.concord_solver_estimate_entries(self._h, ctypes.byref(cnt), _lib.ptr(ii), _lib.ptr(jj),
+                                                     _lib.ptr(vv), k))
+        return ii, jj, vv
+
     def fit(self, lam, delta_tol=1e-5, max_iter=200, init=None, trace=True, raise_on_cap=True) -> FitReport:
         rc, res, deltas, objs, secs = self.fit_raw(lam, delta_tol, max_iter, init, trace)
         om = self.omega()

@@ -271,3 +271,36 @@ def test_virtual_shards_consecutive_fits_and_large_p(oracle):
     ref = oracle.pcd_fit(t, 1000, 0.25, 1e-5, 500, workers=8, trace=False)
     assert ref["iterations"] == b.iterations
     assert_close_support(b.estimate.omega, ref["omega"])
+
+
+# ------------------------------------------------ device diagnostics (8f #2, #3)
+
+
+@pytest.mark.parametrize("name", ["ar2_p100_n50_l0.3", "sf_p101_n50_l0.3", "ar2_p12_n60_l0.1_tol1e-8"])
+def test_device_check_optimality_and_entries(golden, name, tmp_path):
+    """check_optimality from the maintained W (= Omega T up to rounding) and the
+    device-compacted estimate entries, against the reference's own outputs."""
+    import os
+
+    from paper_2106_09382_b200 import fileio
+    from conftest import REPO
+
+    io = np.load(os.path.join(REPO, "tests", "golden", "reference_io_golden.npz"))
+    c = case(golden, name)
+    with cb.Solver(c["p"]) as s:
+        s.set_gram(cb.GramMatrix(c["t"], c["n"]))
+        rep = s.fit(c["lam"], c["tol"], 5000)
+        opt = s.check_optimality(c["lam"])
+        ents = s.estimate_entries()
+    worst, i, j = io[f"{name}_opt"]
+    host = cb.check_optimality(rep.estimate, cb.GramMatrix(c["t"], c["n"]), c["lam"])
+    assert abs(opt.worst_violation - host.worst_violation) <= 1e-9 * max(1.0, host.worst_violation)
+    assert opt.worst_coordinate == host.worst_coordinate
+    assert abs(opt.worst_violation - worst) <= 1e-6 * max(1.0, abs(worst))
+    h = fileio.estimate_entries(rep.estimate)
+    for a, b in zip(ents, h):
+        assert np.array_equal(a, b)
+    path = tmp_path / "e.txt"
+    fileio.write_estimate(str(path), ents, c["lam"], rep.iterations, rep.final_delta, p=c["p"])
+    est, _ = fileio.read_estimate(str(path))
+    assert np.array_equal(est.omega, rep.estimate.omega)
