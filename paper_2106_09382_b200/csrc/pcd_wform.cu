@@ -200,9 +200,27 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
 // stores visible (GPU scope, or system scope when the shards are separate
 // GPUs reached over NVLink), then bump every copy of the arrival counter.
 __device__ __forceinline__ void arrive_all(const WformArgs& a) {
-    if (a.sys_scope) __threadfence_system();
-    else __threadfence();
-    FOR_COPIES_A(r) atomicAdd(a.x.bar[r], 1ull);
+    if (a.sys_scope) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        FOR_COPIES_A(r) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
+    } else if (a.G == 1) {
+        // release-reduction: MEMBAR.ALL.GPU + REDG (no sequentially-consistent fence, no L1 invalidate)
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[0]) : "memory");
+    } else {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        FOR_COPIES_A(r) asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
+    }
+}
+
+// Wait until the barrier counter reaches `target`: relaxed polling (a plain L2
+// load per iteration, no L1 invalidate per poll), then one acquire fence.
+__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target, int sys) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+    if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 struct Smem {
@@ -330,8 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             long long t0 = clock64();
             if (tc == 0) {
                 const unsigned long long target = a.bar_base + (unsigned long long)(g + 1) * (unsigned long long)nblk;
-                while (ld_acquire_u64(barL) < target) {
-                }
+                wait_counter(barL, target, a.sys_scope);
                 st_vol(&s_epoch, g);
             }
             bar_chain();

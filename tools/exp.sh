@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
+export CONCORD_PHASE_PROFILE=1
+timeout 60 python tools/profile_fit.py --p 5000 --n 2000 --lam 0.3 --fits 1 > gpurun_out/phase_03.log 2>&1
+timeout 60 python tools/profile_fit.py --p 5000 --n 2000 --lam 0.1 --fits 1 > gpurun_out/phase_01.log 2>&1
+timeout 60 python tools/profile_fit.py --p 1000 --n 500 --lam 0.3 --fits 1 > gpurun_out/phase_1000.log 2>&1
+unset CONCORD_PHASE_PROFILE
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" > gpurun_out/status.txt
-timeout 300 compute-sanitizer --tool memcheck python -m pytest tests -x -q -m gpu -k "device_check_optimality" > gpurun_out/memcheck_diag.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/status.txt
