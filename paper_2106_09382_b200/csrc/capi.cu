@@ -583,6 +583,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     if (const char* e = getenv("CONCORD_STAGE_AHEAD")) a.stage_ahead = atoi(e);
     if (a.stage_ahead < 2) a.stage_ahead = 2;
     if (a.stage_ahead > 3) a.stage_ahead = 3;
+    a.tdiag_smem = wform_tdiag_in_smem(s->p);
     a.status = s->status;
     unsigned long long* prof = nullptr;
     const bool want_prof = getenv("CONCORD_PHASE_PROFILE") != nullptr;
@@ -642,11 +643,12 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         const double ph = (double)pc[3];
         fprintf(stderr, "[concord phase profile] p=%d iters=%d phases=%.0f lmax=%d shards=%d clk=%d kHz (CTA 0)\n",
                 s->p, iters, ph, s->lmax, s->G, clk_khz);
-        const char* names[12] = {"chain: barrier wait", "chain: stage wait", "chain: publish+share+arrive", "-",
+        const char* names[15] = {"chain: barrier wait", "chain: stage wait", "chain: publish+share+arrive", "-",
                                  "apply: busy", "apply: idle", "apply: batches", "chain:  publish (tc0)",
                                  "chain:  bar+fence+arrive", "chain:  share (last thread)", "apply:  heads+stage",
-                                 "apply:  diagonal steps"};
-        for (int i = 0; i < 12; ++i) {
+                                 "apply:  diagonal steps", "apply:   broadcast bars", "apply:   heads loop (ta0)",
+                                 "apply:   stage loop (ta0)"};
+        for (int i = 0; i < 15; ++i) {
             if (i == 3 || i == 6) continue;
             const double us = pc[i] / (clk_khz * 1e-3);
             fprintf(stderr, "  %-30s %12.1f us total  %9.3f us/phase\n", names[i], us, us / (ph > 0 ? ph : 1));

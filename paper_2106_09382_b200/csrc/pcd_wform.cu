@@ -180,8 +180,8 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
                     const int dst = h ? rs.y : rs.x;
                     const int src = h ? rs.x : rs.y;
                     wp[u] = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
-                    tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
-                    wv[u] = *wp[u];
+                    tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
+                    wv[u] = __ldcg(wp[u]);
                 }
             }
         }
@@ -231,6 +231,7 @@ struct Smem {
     double* L_new;  // [kPairCap]  (diag chunk: new value)
     int* L_ph;      // [kPairCap]  batch phase of each entry
     unsigned* bm;   // [(p + 31) / 32] row bitmap of a chunk (conflict detection)
+    double* td;     // [p] T diagonal in shared memory (small p), or NULL
 };
 
 __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             dmaxL = a.x.dmax[r];
         }
     const int ssz = (2 + lmax) * w;  // doubles per stage slot
+#define TD(i) (sm.td ? sm.td[i] : __ldg(a.tdiag + (i)))
 
     Smem sm;
     {
@@ -296,7 +298,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         sm.s_off = reinterpret_cast<int*>(ptr);
         ptr += sizeof(int) * ((size_t)kBatch * nblk + 1);
         sm.bm = reinterpret_cast<unsigned*>(ptr);
+        ptr += sizeof(unsigned) * (size_t)((p + 31) / 32);
+        ptr = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ptr) + 15) & ~(uintptr_t)15);
+        sm.td = a.tdiag_smem ? reinterpret_cast<double*>(ptr) : nullptr;
     }
+    if (sm.td)
+        for (int i = tid; i < p; i += kThreads) sm.td[i] = __ldg(a.tdiag + i);
     for (int i = tid; i < (p + 31) / 32; i += kThreads) sm.bm[i] = 0u;
 
     // ---- initial stages: publish phases 0..min(2, lmax) from the initial W (watermark -1)
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             st[w + j] = Ob[(long long)x * w + j];
             for (int i = 0; i < Q; ++i) {  // phases k = 0 .. Q-1 not covered by the stage
                 const int y = src_row(i, x, m);
-                st[(2 + i) * w + j] = (y < p) ? __ldg(Tb + (long long)y * w + j) : 0.0;
+                st[(2 + i) * w + j] = (y < p) ? __ldcg(Tb + (long long)y * w + j) : 0.0;
             }
         }
     }
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 double dm = 0.0;
                 for (int i = tc; i < p; i += kChain) {
                     const double2 v = ldcg2(pb + i);
-                    const double nv = diag_from_dot(v.x, v.y, __ldg(a.tdiag + i), a.n);
+                    const double nv = diag_from_dot(v.x, v.y, TD(i), a.n);
                     const double d = __dsub_rn(nv, v.y);
                     dd[i] = make_double2(d, nv);
                     if ((unsigned)(i - c0) < (unsigned)wl)
@@ -425,7 +432,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         dk[i] = (i < L - 1) ? __ldcg(dringL + (size_t)(k % a.rd) * p + x) : 0.0;
                     }
                     const int y = src_row(ph, x, m);
-                    const double dlast = (y < p) ? row_delta(ph, x, y, pb, a.tdiag, m, a.shrink, a.n) : 0.0;
+                    double dlast = 0.0;
+                    if (y < p) {
+                        if (ph < m) {
+                            const int r = min(x, y), s2 = max(x, y);
+                            double nv_;
+                            dlast = pair_delta(ldcg2(pb + r), ldcg2(pb + s2), TD(r), TD(s2), a.shrink, nv_);
+                        } else {
+                            const double2 v = ldcg2(pb + x);
+                            dlast = __dsub_rn(diag_from_dot(v.x, v.y, TD(x), a.n), v.y);
+                        }
+                    }
                     double val = st[j];
                     const double om = st[w + j];
 #pragma unroll
@@ -452,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     if (q < q_hi) {
                         round_pair(q, m, c1, r, s);
                         if (s < p) {
-                            d = pair_delta(ldcg2(pb + r), ldcg2(pb + s), __ldg(a.tdiag + r), __ldg(a.tdiag + s),
+                            d = pair_delta(ldcg2(pb + r), ldcg2(pb + s), TD(r), TD(s),
                                            a.shrink, nv);
                             FOR_COPIES(c) {
                                 a.x.dring[c][dg_off + r] = d;
@@ -541,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         int cit = -1;          // sweep of C
         int staged = init_hi;  // highest publish phase staged
         int nbmax = kBatch;    // phases per batch (1 after a dense batch)
-        long long t_busy = 0, t_idle = 0, nbatch = 0, t_head = 0, t_diag = 0;
+        long long t_busy = 0, t_idle = 0, nbatch = 0, t_head = 0, t_diag = 0, t_h0 = 0, t_h1 = 0, t_h2 = 0;
         while (true) {
             const long long t0 = clock64();
             bar_apply();  // everyone has consumed the previous broadcast
@@ -575,6 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 continue;
             }
 
+            const long long ta0 = clock64();
             // ---- one round trip: segment heads (count + first entry) and the stage cells
             for (int idx = ta; idx < nseg; idx += kApply) {
                 const int jb = idx / nsh;
@@ -597,6 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
                 }
             }
+            const long long ta1 = clock64();
             for (int idx = ta; idx < nq * wl; idx += kApply) {
                 const int qi = idx / wl, j = idx - qi * wl;
                 const int Q = staged + 1 + qi;
@@ -604,25 +623,55 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 if (x < 0) continue;
                 double* st = sm.stage + (size_t)(Q % kSlots) * ssz;
                 const int L = Q - 1 - C;
-                double tv[kMaxLag];
-                int phk = ph0;  // phase-in-sweep of C+1
+                // source rows of phases C+1 .. Q-1 for row x, stepped without integer division
+                // (partner_{k+1}(x) = partner_k(x) - 2 mod m for x >= 1, -1 for x == 0)
+                int ys[kMaxLag];
+                {
+                    int phk = ph0;  // phase-in-sweep of C+1
+                    int y = (phk < m) ? circle_partner(x, phk, m) : x;
+                    const int step = (x == 0) ? 1 : 2;
 #pragma unroll
-                for (int i = 0; i < kMaxLag; ++i) {
-                    const int y = src_row(phk, x, m);
-                    tv[i] = (i < L && y < p) ? __ldg(Tb + (long long)y * w + j) : 0.0;
-                    phk = (phk == m) ? 0 : phk + 1;
+                    for (int i = 0; i < kMaxLag; ++i) {
+                        ys[i] = (i < L && y < p) ? y : -1;
+                        // advance to phase phk + 1
+                        if (phk == m) {
+                            phk = 0;
+                            y = circle_partner(x, 0, m);
+                        } else if (phk == m - 1) {
+                            phk = m;
+                            y = x;
+                        } else {
+                            ++phk;
+                            if (x == 0) {
+                                y = (y == 1) ? m : y - 1;
+                            } else {
+                                // the self-mapped position becomes 0; undo before stepping
+                                int yy = (y == 0) ? x : y;
+                                yy -= step;
+                                if (yy < 1) yy += m;
+                                y = (yy == x) ? 0 : yy;
+                            }
+                        }
+                    }
                 }
-                const double wv = Wb[(long long)x * w + j];
-                const double ov = Ob[(long long)x * w + j];
+                double tv[kMaxLag];
+#pragma unroll
+                for (int i = 0; i < kMaxLag; ++i) tv[i] = __ldcg(Tb + (long long)(ys[i] >= 0 ? ys[i] : x) * w + j);
+                const double wv = __ldcg(Wb + (long long)x * w + j);
+                const double ov = __ldcg(Ob + (long long)x * w + j);
                 st[j] = wv;
                 st[w + j] = ov;
 #pragma unroll
                 for (int i = 0; i < kMaxLag; ++i)
-                    if (i < L) st[(2 + i) * w + j] = tv[i];
+                    if (i < L) st[(2 + i) * w + j] = (ys[i] >= 0) ? tv[i] : 0.0;
             }
             for (int Q = staged + 1 + ta; Q <= target; Q += kApply) s_stbase[Q % kSlots] = C;
+            const long long ta2 = clock64();
             bar_apply();
             t_head += clock64() - t0;
+            t_h0 += ta0 - t0;
+            t_h1 += ta1 - ta0;
+            t_h2 += ta2 - ta1;
             if (nq > 0) {
                 staged = target;
                 if (ta == 0) {
@@ -653,8 +702,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                                 const int ii = idx / w2;
                                 const int j2 = idx - ii * w2;
                                 const long long off = (long long)(i0 + ii) * w + 2 * j2;
-                                wv[u] = *reinterpret_cast<const double2*>(Wb + off);
-                                if (sm.L_d[ii] != 0.0) tv[u] = __ldg(reinterpret_cast<const double2*>(Tb + off));
+                                wv[u] = __ldcg(reinterpret_cast<const double2*>(Wb + off));
+                                if (sm.L_d[ii] != 0.0) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + off));
                                 if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
                             }
                         }
@@ -826,6 +875,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             prof[6] = (unsigned long long)nbatch;
             prof[10] = (unsigned long long)t_head;
             prof[11] = (unsigned long long)t_diag;
+            prof[12] = (unsigned long long)t_h0;
+            prof[13] = (unsigned long long)t_h1;
+            prof[14] = (unsigned long long)t_h2;
         }
     }
     __syncthreads();
@@ -923,6 +975,8 @@ __global__ void wform_init_csr_kernel(const int* __restrict__ rowptr, const int*
 
 
 // ------------------------------------------------------------------ launchers
+int wform_tdiag_in_smem(int p) { return p <= 12288; }
+
 int wform_lag_cap(int w, int m) {
     int l = WFORM_MAX_LAG < m ? WFORM_MAX_LAG : m;
     while (l > 1 && (size_t)kSlots * (2 + l) * w * sizeof(double) > 150 * 1024) --l;
@@ -935,6 +989,8 @@ size_t wform_smem_bytes(int w, int p, int nblk, int lmax) {
     b += sizeof(int) * ((size_t)kBatch * nblk + 1);
     b = (b + 15) & ~(size_t)15;
     b += sizeof(unsigned) * (size_t)((p + 31) / 32);
+    b = (b + 15) & ~(size_t)15;
+    if (wform_tdiag_in_smem(p)) b += sizeof(double) * (size_t)p;
     return b;
 }
 

@@ -76,12 +76,14 @@ struct WformArgs {
     int share;                      // pairs per share CTA per colour
     int nsh;                        // CTAs that evaluate closed forms (ceil(half / share))
     int stage_ahead;                // publishes staged beyond the chain's phase
+    int tdiag_smem;                 // 1: the T diagonal is copied into shared memory
     int* status;                    // [0] iterations, [1] converged
     unsigned long long* prof;       // optional [16] cycle counters (CTA 0), or NULL
 };
 
 // Lag cap for a slab width (bounded by the stage ring's shared memory) and m.
 int wform_lag_cap(int w, int m);
+int wform_tdiag_in_smem(int p);
 size_t wform_smem_bytes(int w, int p, int nblk, int lmax);
 
 cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st);
