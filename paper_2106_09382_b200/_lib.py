@@ -154,6 +154,12 @@ def last_error():
 def check(rc, allow=()):
     """Raise ConcordError for a non-zero return code not in `allow`."""
     if rc != CONCORD_OK and rc not in allow:
+        if rc == CONCORD_ERR_ZERO_VARIANCE:
+            from .model import ZeroVarianceColumn
+
+            msg = last_error()
+            col = [int(t) for t in msg.split() if t.isdigit()]
+            raise ZeroVarianceColumn(col[0] if col else -1)
         raise ConcordError(rc, last_error())
     return rc
 
