@@ -57,6 +57,43 @@ __device__ __forceinline__ double diag_from_dot(double dot, double om_ii, double
     return __ddiv_rn(__dadd_rn(-a, __dsqrt_rn(disc)), __dmul_rn(2.0, t_ii));
 }
 
+// Pair q of round k without integer division: c1 = m - 1 - k (common.cuh has the closed form).
+__device__ __forceinline__ void round_pair(int q, int m, int c1, int& r, int& s) {
+    int a, b;
+    if (q == 0) {
+        a = 0;
+        b = 1 + c1;
+    } else {
+        const int t = q + c1;
+        const int u = m + c1 - q;
+        a = 1 + (t >= m ? t - m : t);
+        b = 1 + (u >= m ? u - m : u);
+    }
+    r = min(a, b);
+    s = max(a, b);
+}
+
+// delta of pair (r, s) from the published half values vr = (W[s,r], Om[s,r]),
+// vs = (W[r,s], Om[r,s]); same operation order as offdiag_from_sums, with the
+// division skipped when the soft threshold returns its exact 0.0.
+__device__ __forceinline__ double pair_delta(double2 vr, double2 vs, double trr, double tss, double shrink,
+                                             double& nv) {
+    const double om = vs.y;
+    const double num = -__dsub_rn(__dadd_rn(vs.x, vr.x), __dmul_rn(om, __dadd_rn(tss, trr)));
+    const double av = __dsub_rn(fabs(num), shrink);
+    nv = (av <= 0.0) ? 0.0 : __ddiv_rn(num > 0.0 ? av : -av, __dadd_rn(trr, tss));
+    return __dsub_rn(nv, om);
+}
+
+// Row published for column c in phase ph (ph < m: colour ph, ph == m: diagonal), or -1.
+__device__ __forceinline__ int pub_row(int ph, int c, int m, int p) {
+    const int x = (ph < m) ? circle_partner(c, ph, m) : c;
+    return x < p ? x : -1;
+}
+
+// Row whose value moves row x in phase ph (its pair partner; x itself on the diagonal).
+__device__ __forceinline__ int src_row(int ph, int x, int m) { return ph < m ? circle_partner(x, ph, m) : x; }
+
 // ---------------------------------------------------------------------------
 // Grid-wide barrier for a cooperative (co-resident) launch: one monotonic
 // 64-bit arrival counter, zeroed by the host before each launch.  `target` is
