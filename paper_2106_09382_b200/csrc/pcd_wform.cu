@@ -81,6 +81,11 @@ __device__ __forceinline__ void bar_chain() { asm volatile("bar.sync 1, %0;" ::"
 __device__ __forceinline__ void bar_apply() { asm volatile("bar.sync 2, %0;" ::"n"(kApply) : "memory"); }
 
 __device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
 
 // Exclusive scan of s[0..n) in place by the apply warps; returns the total (also in s[n]).
@@ -374,9 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 const int phQ = (ph == m) ? 0 : ph + 1;
                 const int slot = Q % kSlots;
                 if (tc < wl) {
-                    while (ld_vol(&s_staged) < Q) {
+                    while (ld_acquire_cta(&s_staged) < Q) {
                     }
-                    __threadfence_block();
                 }
                 long long t2 = clock64();
                 t_stage += t2 - t1;
@@ -386,24 +390,30 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     const int c = c0 + j;
                     const int x = pub_row(phQ, c, m, p);
                     if (x < 0) continue;
+                    // phase-g delta of row x from the phase-g publish buffer (loads issued first)
+                    const int y = src_row(ph, x, m);
+                    double2 vr = make_double2(0.0, 0.0), vs = vr;
+                    if (y < p) {
+                        vr = ldcg2(pb + (ph < m ? min(x, y) : x));
+                        if (ph < m) vs = ldcg2(pb + max(x, y));
+                    }
                     const int C = ld_vol(&s_stbase[slot]);
                     const int L = g - C;  // phases C+1 .. g, L >= 1
                     double dk[kMaxLag];
+                    int kslot = (C + 1) % a.rd;
 #pragma unroll
                     for (int i = 0; i < kMaxLag; ++i) {
-                        const int k = C + 1 + i;
-                        dk[i] = (i < L - 1) ? __ldcg(dringL + (size_t)(k % a.rd) * p + x) : 0.0;
+                        dk[i] = (i < L - 1) ? __ldcg(dringL + (size_t)kslot * p + x) : 0.0;
+                        kslot = (kslot + 1 == a.rd) ? 0 : kslot + 1;
                     }
-                    const int y = src_row(ph, x, m);
                     double dlast = 0.0;
                     if (y < p) {
                         if (ph < m) {
                             const int r = min(x, y), s2 = max(x, y);
                             double nv_;
-                            dlast = pair_delta(ldcg2(pb + r), ldcg2(pb + s2), TD(r), TD(s2), a.shrink, nv_);
+                            dlast = pair_delta(vr, vs, TD(r), TD(s2), a.shrink, nv_);
                         } else {
-                            const double2 v = ldcg2(pb + x);
-                            dlast = __dsub_rn(diag_from_dot(v.x, v.y, TD(x), a.n), v.y);
+                            dlast = __dsub_rn(diag_from_dot(vr.x, vr.y, TD(x), a.n), vr.y);
                         }
                     }
                     double val = st[j];
