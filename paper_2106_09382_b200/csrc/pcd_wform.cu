@@ -63,6 +63,10 @@ constexpr int kBatch = WFORM_BATCH;
 constexpr int kSlots = WFORM_STAGE_SLOTS;
 constexpr int kMaxLag = WFORM_MAX_LAG;
 constexpr int kUnroll = 2;
+#ifndef WFORM_ROW_UNROLL
+#define WFORM_ROW_UNROLL 2
+#endif
+constexpr int kRowUnroll = WFORM_ROW_UNROLL;  // row-stream items in flight per thread (bytes in flight / SM)
 
 // Phase-ph delta of row x (paired with y) recomputed from that phase's publish buffer.
 __device__ __forceinline__ double row_delta(int ph, int x, int y, const double2* pb, const double* tdiag, int m,
@@ -129,12 +133,12 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
     const int w = 2 * w2;
     const int per = 2 * w2;
     const int items = (e_hi - e_lo) * per;
-    for (int base = 0; base < items; base += kApply * kUnroll) {
-        double2 tv[kUnroll], wv[kUnroll];
-        double2* wp[kUnroll];
-        double dd[kUnroll];
+    for (int base = 0; base < items; base += kApply * kRowUnroll) {
+        double2 tv[kRowUnroll], wv[kRowUnroll];
+        double2* wp[kRowUnroll];
+        double dd[kRowUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < kRowUnroll; ++u) {
             const int idx = base + u * kApply + ta;
             wp[u] = nullptr;
             if (idx < items) {
@@ -154,7 +158,7 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
             }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < kRowUnroll; ++u) {
             if (wp[u]) {
                 wv[u].x = fma(dd[u], tv[u].x, wv[u].x);
                 wv[u].y = fma(dd[u], tv[u].y, wv[u].y);
