@@ -1,8 +1,8 @@
 mkdir -p gpurun_out
-for v in base u2 u8; do
-  if [ $v = base ]; then lib=paper_2106_09382_b200/libconcord_b200.so; else lib=build/lib_$v.so; fi
-  for cfg in "--p 5000 --n 2000 --lam 0.3" "--p 5000 --n 2000 --lam 0.15" "--p 5000 --n 2000 --lam 0.1" "--p 5000 --n 2000 --lam 0.0 --max-iter 2"; do
-    echo "== $v $cfg" >> gpurun_out/ab.log
-    CONCORD_LIB_PATH=$lib timeout 60 python tools/profile_fit.py $cfg --fits 1 2>&1 | grep -E "fit lam|Error" | sed 's/per-sweep.*//' >> gpurun_out/ab.log
-  done
-done
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --format=csv > gpurun_out/gpu.txt 2>&1; nproc >> gpurun_out/gpu.txt
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" > gpurun_out/status.txt
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/status.txt
+timeout 900 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 0 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?" >> gpurun_out/status.txt
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:pcd_wform --clock-control none --csv --log-file gpurun_out/traffic.csv python tools/ncu_fits.py > gpurun_out/ncu_traffic.log 2>&1; echo "traffic rc=$?" >> gpurun_out/status.txt
+timeout 900 ncu --set full --import-source on -k regex:pcd_wform --clock-control none -c 1 -o gpurun_out/prof_wform_r01_final python tools/ncu_fits.py --lams 0.3 --out gpurun_out/ncu_fit03.json > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?" >> gpurun_out/status.txt
