@@ -143,6 +143,13 @@ int concord_solver_estimate_entries(concord_solver* s, int64_t* count, int32_t* 
  * min(cap, iterations) entries, *count = iterations of the last fit. */
 int concord_solver_sweep_stats(concord_solver* s, int64_t* nnz_pairs, int32_t cap, int32_t* count);
 
+/* ---- synthetic data on the device ------------------------- */
+/* Centred samples of N(0, inv(ar2_precision(p))) (datagen.py:64-78, 135-154):
+ * same distribution as the reference sampler, a counter-based (Philox) random
+ * stream, O(p n) work, no host copy of X when the Gram is built in place. */
+int concord_ar2_data_f64(int64_t p, int64_t n, uint64_t seed, double* X_out, int32_t where, int32_t device);
+int concord_solver_gram_from_ar2(concord_solver* s, int64_t n, uint64_t seed);
+
 /* ---- pinned host buffers for fast H2D/D2H of T and Omega ---------------- */
 int concord_host_alloc(int64_t bytes, void** out);
 int concord_host_free(void* ptr);

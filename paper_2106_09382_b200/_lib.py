@@ -32,6 +32,7 @@ EXPORTS = (
     "concord_solver_create_sharded", "concord_solver_layout", "concord_shard_create",
     "concord_shard_ipc_handle", "concord_shard_open_peers", "concord_solver_objective_parts",
     "concord_solver_check_optimality", "concord_solver_estimate_entries",
+    "concord_ar2_data_f64", "concord_solver_gram_from_ar2",
 )
 
 ABI_VERSION = 2
@@ -138,6 +139,8 @@ def load(build_if_missing=True):
             "concord_solver_check_optimality": ([vp, d, ctypes.POINTER(d), ctypes.POINTER(i64), ctypes.POINTER(i64)],
                                                 ctypes.c_int),
             "concord_solver_estimate_entries": ([vp, ctypes.POINTER(i64), vp, vp, vp, i64], ctypes.c_int),
+            "concord_ar2_data_f64": ([i64, i64, ctypes.c_uint64, vp, i32, i32], ctypes.c_int),
+            "concord_solver_gram_from_ar2": ([vp, i64, ctypes.c_uint64], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -795,6 +795,80 @@ int concord_solver_estimate_entries(concord_solver* s, int64_t* count, int32_t* 
     return CONCORD_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Banded Cholesky of the AR(2) truth (unit diagonal, bands 0.45 / 0.40; datagen.py:64-78):
+// lb[k*p + i] = L[i+k, i].
+int ar2_factor(int p, std::vector<double>& lb) {
+    lb.assign(3 * (size_t)p, 0.0);
+    for (int i = 0; i < p; ++i) {
+        const double a1 = (i >= 1) ? lb[p + (i - 1)] : 0.0;      // L[i, i-1]
+        const double a2 = (i >= 2) ? lb[2 * p + (i - 2)] : 0.0;  // L[i, i-2]
+        const double d = 1.0 - a1 * a1 - a2 * a2;
+        if (!(d > 0.0)) return fail(CONCORD_ERR_ARG, "AR(2) truth is not positive definite at %d", i);
+        const double lii = sqrt(d);
+        lb[i] = lii;
+        if (i + 1 < p) {
+            const double l_i1_im1 = (i >= 1) ? lb[2 * p + (i - 1)] : 0.0;  // L[i+1, i-1]
+            lb[p + i] = (0.45 - l_i1_im1 * a1) / lii;
+        }
+        if (i + 2 < p) lb[2 * p + i] = 0.40 / lii;
+    }
+    return CONCORD_OK;
+}
+
+// Centred AR(2) samples on the device: X_dev (n x p). Scratch is allocated here.
+int ar2_sample_device(int p, long long n, unsigned long long seed, double* X_dev, cudaStream_t st) {
+    std::vector<double> lb;
+    int rc = ar2_factor(p, lb);
+    if (rc) return rc;
+    double *dlb = nullptr, *XT = nullptr, *mean = nullptr;
+    cudaError_t e = dalloc(&dlb, lb.size());
+    if (e == cudaSuccess) e = dalloc(&XT, (size_t)n * p);
+    if (e == cudaSuccess) e = dalloc(&mean, p);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dlb, lb.data(), sizeof(double) * lb.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch_ar2_sample(dlb, p, n, seed, XT, mean, X_dev, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dlb);
+    cudaFree(XT);
+    cudaFree(mean);
+    CK(e);
+    return CONCORD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int concord_ar2_data_f64(int64_t p, int64_t n, uint64_t seed, double* X_out, int32_t where, int32_t device) {
+    if (!X_out || p < 3 || n < 1) return fail(CONCORD_ERR_ARG, "need p >= 3, n >= 1 and an output buffer");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    double* Xd = X_out;
+    if (where == CONCORD_HOST) CK(dalloc(&Xd, (size_t)n * p));
+    rc = ar2_sample_device((int)p, n, seed, Xd, nullptr);
+    if (!rc && where == CONCORD_HOST) {
+        cudaError_t e = cudaMemcpy(X_out, Xd, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = fail(CONCORD_ERR_CUDA, "copy: %s", cudaGetErrorString(e));
+    }
+    if (where == CONCORD_HOST) cudaFree(Xd);
+    return rc;
+}
+
+int concord_solver_gram_from_ar2(concord_solver* s, int64_t n, uint64_t seed) {
+    if (!s || n < 1 || s->p < 3) return fail(CONCORD_ERR_ARG, "bad arguments");
+    DeviceGuard g(s->dev);
+    double* X = nullptr;
+    CK(dalloc(&X, (size_t)n * s->p));
+    int rc = ar2_sample_device(s->p, n, seed, X, s->stream);
+    if (!rc) rc = concord_solver_gram_from_data(s, X, n, CONCORD_DEVICE);
+    cudaFree(X);
+    return rc;
+}
+
 int concord_host_alloc(int64_t bytes, void** out) {
     if (!out || bytes < 0) return fail(CONCORD_ERR_ARG, "bad arguments");
     *out = nullptr;

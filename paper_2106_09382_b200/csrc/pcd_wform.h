@@ -117,6 +117,10 @@ cudaError_t launch_triplet_count(const double* Om, int p, int w, int* rowcnt, cu
 cudaError_t launch_triplet_write(const double* Om, int p, int w, const long long* rowoff, int* ti, int* tj,
                                  double* tv, cudaStream_t st);
 
+// On-device AR(2) samples (datagen.cu): centred X (n x p row-major); XT (p x n) and mean (p) are scratch.
+cudaError_t launch_ar2_sample(const double* lb, int p, long long n, unsigned long long seed, double* XT, double* mean,
+                              double* X, cudaStream_t st);
+
 // FP64 DMMA Gram / GEMM, gram.cu.  T = X^T X (X: n x p row-major, leading dim ldx).
 // out_mode 0: row-major p x p (ld = p); 1: slab-major with width w.
 cudaError_t launch_gram_f64(const double* X, long long n, int p, long long ldx, double* out, int out_mode, int w,

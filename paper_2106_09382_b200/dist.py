@@ -163,6 +163,11 @@ class ShardedSolver:
         _lib.check(_lib.load().concord_solver_gram_from_data(self._h, _lib.ptr(x.values), x.n, _lib.HOST))
         self.n = x.n
 
+    def gram_from_ar2(self, n, seed=0):
+        """T from n AR(2) samples drawn on this GPU (counter-based stream: every rank draws the same X)."""
+        _lib.check(_lib.load().concord_solver_gram_from_ar2(self._h, int(n), int(seed)))
+        self.n = int(n)
+
     def omega_block(self):
         out = np.empty((self.p, self.ncols))
         _lib.check(_lib.load().concord_solver_get_omega(self._h, _lib.ptr(out), _lib.HOST))

@@ -217,6 +217,11 @@ class Solver:
         _lib.check(_lib.load().concord_solver_gram_from_data(self._h, _lib.ptr(x.values), x.n, _lib.HOST))
         self.n = x.n
 
+    def gram_from_ar2(self, n, seed=0):
+        """T of n centred AR(2) samples generated on the device (no host copy of X)."""
+        _lib.check(_lib.load().concord_solver_gram_from_ar2(self._h, int(n), int(seed)))
+        self.n = int(n)
+
     def gram(self) -> GramMatrix:
         t = np.empty((self.p, self.p))
         _lib.check(_lib.load().concord_solver_get_gram(self._h, _lib.ptr(t), _lib.HOST))

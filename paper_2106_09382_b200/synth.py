@@ -106,6 +106,19 @@ def sample_mvn_ar2_banded(p, n, seed=0):
     return np.ascontiguousarray(x)
 
 
+def sample_ar2_device(p, n, seed=0, device=0):
+    """Centred N(0, inv(ar2_precision(p))) samples drawn on the GPU (csrc/datagen.cu).
+
+    Same distribution as center(sample_mvn(ar2_precision(p), n, seed)), a
+    different (Philox) random stream; O(p n) work on the device.
+    """
+    from . import _lib
+
+    x = np.empty((n, p))
+    _lib.check(_lib.load().concord_ar2_data_f64(int(p), int(n), int(seed), _lib.ptr(x), _lib.HOST, int(device)))
+    return x
+
+
 def center(x):
     """model.py:182-187 (center_columns on a raw array)."""
     return x - x.mean(axis=0)

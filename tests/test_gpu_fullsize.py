@@ -69,3 +69,24 @@ def test_zero_variance_column_is_reported():
         cb.compute_gram(cb.DataMatrix(x))
     with cb.Solver(6) as s, pytest.raises(cb.ZeroVarianceColumn):
         s.gram_from_data(cb.DataMatrix(x))
+
+
+def test_device_ar2_sampler_moments():
+    """synth.sample_ar2_device (csrc/datagen.cu) draws N(0, inv(ar2_precision(p))):
+    centred, sample covariance within sampling error of the truth's inverse
+    (the reference's sampler moment checks, test_datagen.py:113-151)."""
+    p, n = 40, 200_000
+    x = synth.sample_ar2_device(p, n, seed=3)
+    assert x.shape == (n, p)
+    assert np.max(np.abs(x.mean(axis=0))) < 1e-12
+    sigma = np.linalg.inv(synth.ar2_precision(p))
+    s = x.T @ x / n
+    assert np.max(np.abs(s - sigma)) < 6.0 * np.max(np.abs(sigma)) / np.sqrt(n)
+    x2 = synth.sample_ar2_device(p, n, seed=3)
+    assert np.array_equal(x, x2)  # counter-based stream: reproducible
+    assert not np.array_equal(x, synth.sample_ar2_device(p, n, seed=4))
+    # the Gram built on the device from the same draws equals the Gram of the host copy
+    with cb.Solver(p) as s1:
+        s1.gram_from_ar2(n, seed=3)
+        g = s1.gram()
+    np.testing.assert_allclose(g.t, synth.host_gram(x), rtol=1e-12, atol=1e-9)
