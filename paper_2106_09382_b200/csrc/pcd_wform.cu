@@ -534,7 +534,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         int cph = m;           // phase-in-sweep of C (C = -1 behaves like a diagonal step)
         int cit = -1;          // sweep of C
         int staged = init_hi;  // highest publish phase staged
-        int nbmax = kBatch;    // phases per batch (1 after a dense batch)
         long long t_busy = 0, t_idle = 0, nbatch = 0, t_head = 0, t_diag = 0, t_h0 = 0, t_h1 = 0, t_h2 = 0;
         while (true) {
             const long long t0 = clock64();
@@ -556,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             const int it0 = (cph == m) ? cit + 1 : cit;
             const bool have = C < avail;
             const bool diag = have && ph0 == m;
-            const int k1 = (have && !diag) ? min(min(avail, k0 + nbmax - 1), k0 + (m - 1 - ph0)) : C;
+            const int k1 = (have && !diag) ? min(min(avail, k0 + kBatch - 1), k0 + (m - 1 - ph0)) : C;
             const int nb = k1 - C;  // colour phases in this batch (0 for none / diagonal)
             const int nsh = a.nsh;
             const int nseg = nb * nsh;
@@ -837,7 +836,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         if (ta == 0) s_conflict = 0;
                     }
                 }
-                nbmax = (total > 256) ? 1 : kBatch;
                 C = k1;
                 cph = ph0 + (k1 - k0);
                 cit = it0;
