@@ -106,6 +106,15 @@ struct concord_solver {
     int nblk_launch = 0;  // slabs (CTAs) this solver launches
     long long slab = 0;
     int lmax = 1, rd = 0, rl = 0, share = 0, nsh = 0;
+    bool qb = false;       // temporally blocked chain (pcd_qblock.cu)
+    int qb_D = 0, qb_NB = 0, qb_sr = 0, qb_rd = 0, qb_rl = 0;
+    double* qb_stW = nullptr;
+    double* qb_stO = nullptr;
+    double2* qb_diagv = nullptr;
+    double* qb_dring = nullptr;
+    int2* qb_lrs = nullptr;
+    double2* qb_ldn = nullptr;
+    int* qb_lcnt = nullptr;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     double* T = nullptr;
@@ -271,6 +280,33 @@ WformCopies copies(const concord_solver* s) {
     return x;
 }
 
+// Buffers of the temporally blocked chain (pcd_qblock.cu); leaves s->qb false when it does not fit.
+int setup_qblock(concord_solver* s) {
+    const int p = s->p;
+    const int m = p + (p & 1) - 1;
+    int D = QB_DEFAULT_D;
+    if (const char* e = getenv("CONCORD_QB_D")) D = atoi(e);
+    if (D < 1) D = 1;
+    if (D > QB_DMAX) D = QB_DMAX;
+    if (2 * D > m + 1) D = (m + 1) / 2;
+    const size_t smem = qblock_smem_bytes(p, s->nblk_tot, s->share, D, wform_tdiag_in_smem(p));
+    if (smem > 227 * 1024) return CONCORD_OK;  // stays on the per-phase kernel
+    s->qb_D = D;
+    s->qb_NB = (m + 1 + D - 1) / D;
+    s->qb_sr = 4 * D + 4;
+    s->qb_rd = 8 * D + 8;
+    s->qb_rl = 10 * D + 8;
+    CK(dalloc(&s->qb_stW, (size_t)s->qb_sr * p));
+    CK(dalloc(&s->qb_stO, (size_t)s->qb_sr * p));
+    CK(dalloc(&s->qb_diagv, p));
+    CK(dalloc(&s->qb_dring, (size_t)s->qb_rd * p));
+    CK(dalloc(&s->qb_lrs, (size_t)s->qb_rl * s->nblk_tot * s->share));
+    CK(dalloc(&s->qb_ldn, (size_t)s->qb_rl * s->nblk_tot * s->share));
+    CK(dalloc(&s->qb_lcnt, (size_t)s->qb_rl * s->nblk_tot));
+    s->qb = true;
+    return CONCORD_OK;
+}
+
 // Common constructor: G shards of nblk_loc slabs; rank < 0 keeps every shard on `device`.
 int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards, int32_t rank,
                   concord_solver** out) {
@@ -366,6 +402,14 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
     for (auto& e : s->ev) CKC(cudaEventCreate(&e));
     CKC(cudaStreamSynchronize(s->stream));
 #undef CKC
+    // temporally blocked chain for the single-device unsharded solver
+    bool use_qb = (G == 1 && rank < 0 && n_blocks <= 0 && ip >= 256);
+    if (const char* e = getenv("CONCORD_KERNEL")) use_qb = use_qb && strcmp(e, "qblock") == 0;
+    else use_qb = use_qb && QB_DEFAULT;
+    if (use_qb) {
+        const int rc = setup_qblock(s);
+        if (rc) return cleanup(rc);
+    }
     *out = s;
     return CONCORD_OK;
 }
@@ -453,6 +497,13 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->tdiag);
     cudaFree(s->stage);
     cudaFree(s->diagd);
+    cudaFree(s->qb_stW);
+    cudaFree(s->qb_stO);
+    cudaFree(s->qb_diagv);
+    cudaFree(s->qb_dring);
+    cudaFree(s->qb_lrs);
+    cudaFree(s->qb_ldn);
+    cudaFree(s->qb_lcnt);
     for (int r = 0; r < WFORM_MAX_SHARDS; ++r) {
         if (!s->arena[r]) continue;
         if (s->arena_owned[r]) cudaFree(s->arena[r]);
@@ -592,7 +643,54 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         CK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), s->stream));
     }
     a.prof = prof;
-    CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
+    if (s->qb) {
+        QbArgs q;
+        memset(&q, 0, sizeof(q));
+        q.p = a.p;
+        q.m = a.m;
+        q.half = a.half;
+        q.w = a.w;
+        q.slab = a.slab;
+        q.W = a.W;
+        q.T = a.T;
+        q.Om = a.Om;
+        q.tdiag = a.tdiag;
+        q.tdiag_smem = a.tdiag_smem;
+        q.diagv = s->qb_diagv;
+        q.stW = s->qb_stW;
+        q.stO = s->qb_stO;
+        q.sr = s->qb_sr;
+        q.dring = s->qb_dring;
+        q.rd = s->qb_rd;
+        q.list_rs = s->qb_lrs;
+        q.list_dn = s->qb_ldn;
+        q.list_cnt = s->qb_lcnt;
+        q.rl = s->qb_rl;
+        q.share = s->share;
+        q.bar = a.x.bar[0];
+        q.dmax = a.x.dmax[0];
+        q.bar_base = a.bar_base;
+        q.it_base = a.it_base;
+        q.n = a.n;
+        q.shrink = a.shrink;
+        q.delta_tol = a.delta_tol;
+        q.max_iter = a.max_iter;
+        q.want_trace = a.want_trace;
+        q.D = s->qb_D;
+        q.NB = s->qb_NB;
+        q.cellcap = qblock_cellcap(s->share, s->qb_D);
+        q.rmax = qblock_rmax(s->share, s->qb_D);
+        q.stage_window = 4 * s->qb_D;
+        q.rec_delta = a.rec_delta;
+        q.rec_obj = a.rec_obj;
+        q.rec_time = a.rec_time;
+        q.rec_nnz = a.rec_nnz;
+        q.status = a.status;
+        q.prof = a.prof;
+        CK(launch_pcd_qblock(q, s->nblk_launch, s->stream));
+    } else {
+        CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
+    }
     CK(cudaEventRecord(s->ev[2], s->stream));
     CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->edges, s->stream));
 
@@ -606,7 +704,10 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     // every shard ran the same phases: the barrier saw (phases) * nblk_tot arrivals, one per CTA
     // per phase plus the initial publish, minus the final diagonal step's (no arrival after it)
     const unsigned long long phases = (unsigned long long)iters * (unsigned long long)pe;
-    s->bar_base += phases * (unsigned long long)s->nblk_tot;
+    if (s->qb)  // one arrival per CTA at the start, then one per block up to the deciding block
+        s->bar_base += ((unsigned long long)iters * (unsigned long long)s->qb_NB + 1ull) * (unsigned long long)s->nblk_tot;
+    else
+        s->bar_base += phases * (unsigned long long)s->nblk_tot;
     s->it_base += iters;
     std::vector<double> dl(iters > 0 ? iters : 1);
     std::vector<unsigned long long> tm(iters + 1);

@@ -1,0 +1,895 @@
+// CONCORD-PCD fit kernel with TEMPORAL BLOCKING of the colour chain in pair
+// space (sm_100a).  Same algorithm, arithmetic and results as pcd_wform.cu --
+// bitwise -- with D colour phases per grid barrier instead of one.
+//
+// The circle schedule (schedule.py:68-88) moves every id one position per
+// round, so the pair index q of any row changes by at most one per colour
+// (q = 0 and q = half-1 reflect), and the two rows of a pair share it.  Hence
+// pair q of colour k+1 depends only on pairs q-1, q, q+1 of colour k through
+// the rows it shares with them: a 1-D stencil in q.  A CTA that owns the
+// pairs [q_lo, q_hi) can therefore evaluate D consecutive colours after ONE
+// grid barrier by also evaluating, redundantly, a halo of D-1-d pairs on each
+// side at colour d of the block (identical arithmetic in every CTA that
+// evaluates a pair, so the halo copies agree bit for bit).
+//
+// Per block of D phases (blocks never straddle a sweep; the diagonal phase
+// closes the sweep's last block):
+//  * chain warps: read every cell W[x,c] / Om[x,c] the block's pairs (and
+//    halo) need from the STAGE -- written in global memory by the slab owners
+//    two blocks ahead, already brought forward to the start of the block
+//    before last -- apply the deltas of the two previous blocks (the per-row
+//    delta ring; T entries fetched only where a delta is non-zero) and then,
+//    colour by colour in shared memory, the deltas of this block (T entries
+//    preloaded).  Own pairs write the delta ring and the non-zero delta list;
+//    the diagonal phase writes the (delta, new) vector.  One arrive per block.
+//  * apply warps (as pcd_wform.cu): stream the delta lists into the own slab
+//    in phase order, run the dense diagonal step, and stage the cells of the
+//    block after next at watermark C' = (start of the block before it) - 1,
+//    bringing them forward from their own watermark with exactly the FMAs
+//    they will apply to the slab.
+//
+// Every published value is thus the value of the sequential W-form (same
+// FMAs, same order), and the results equal pcd_wform.cu's bit for bit.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "pcd_wform.h"
+
+namespace concord {
+namespace qb {
+
+constexpr int kThreads = WFORM_THREADS;
+constexpr int kChainWarps = QB_CHAIN_WARPS;
+constexpr int kChain = kChainWarps * 32;
+constexpr int kApply = kThreads - kChain;
+constexpr int kApplyWarps = kApply / 32;
+constexpr int kPairCap = WFORM_PAIR_CAP;
+constexpr int kBatch = WFORM_BATCH;
+constexpr int kUnroll = 2;
+constexpr int kRowUnroll = 2;
+constexpr int kDMax = QB_DMAX;
+
+__device__ __forceinline__ void bar_chain() { asm volatile("bar.sync 1, %0;" ::"n"(kChain) : "memory"); }
+__device__ __forceinline__ void bar_apply() { asm volatile("bar.sync 2, %0;" ::"n"(kApply) : "memory"); }
+__device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+
+// Pair index of id x in round k (position 0 and m form pair 0; position i pairs with m - i).
+__device__ __forceinline__ int pair_of(int x, int k, int m) {
+    if (x == 0) return 0;
+    int pos = x - 1 + k;
+    pos = 1 + (pos >= m ? pos % m : pos);
+    if (pos == m) return 0;
+    return pos < m - pos ? pos : m - pos;
+}
+
+// Geometry of global block b: first global phase g0, its phase-in-sweep ph0, length len.
+struct Blk {
+    int g0, ph0, len, sweep;
+};
+__device__ __forceinline__ Blk block_at(int b, int m, int D, int NB) {
+    Blk k;
+    k.sweep = b / NB;
+    const int j = b - k.sweep * NB;
+    k.ph0 = j * D;
+    k.len = min(D, m + 1 - k.ph0);
+    k.g0 = k.sweep * (m + 1) + k.ph0;
+    return k;
+}
+// Watermark of the stage of block b: every phase <= C' is already in the staged cells.
+__device__ __forceinline__ int stage_mark(int b, int m, int D, int NB) {
+    return (b < 2) ? -1 : block_at(b - 2, m, D, NB).g0 - 1;
+}
+
+// Exclusive scan of s[0..n) in place by the apply warps; returns the total (also in s[n]).
+__device__ int apply_scan(int* s, int n, int ta, int* s_wsum) {
+    const int lane = ta & 31, wa = ta >> 5;
+    const int per = (n + kApply - 1) / kApply;
+    const int lo = min(n, ta * per), hi = min(n, lo + per);
+    int local = 0;
+    for (int i = lo; i < hi; ++i) local += s[i];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[wa] = incl;
+    bar_apply();
+    int wbase = 0, total = 0;
+    for (int j = 0; j < kApplyWarps; ++j) {
+        const int v = s_wsum[j];
+        if (j < wa) wbase += v;
+        total += v;
+    }
+    int run = wbase + incl - local;
+    for (int i = lo; i < hi; ++i) {
+        const int v = s[i];
+        s[i] = run;
+        run += v;
+    }
+    if (ta == 0) s[n] = total;
+    bar_apply();
+    return total;
+}
+
+// Row streams of delta-list entries [e_lo, e_hi) (shared-memory indices; only
+// batch phase `only` when only >= 0): W[dst, own] = fma(d, T[src, own], W[dst, own])
+// for both rows of every pair.
+__device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, const int* L_ph, int only, int e_lo,
+                                           int e_hi, int w2, double* __restrict__ Wb, const double* __restrict__ Tb,
+                                           int ta) {
+    const int w = 2 * w2;
+    const int per = 2 * w2;
+    const int items = (e_hi - e_lo) * per;
+    for (int base = 0; base < items; base += kApply * kRowUnroll) {
+        double2 tv[kRowUnroll], wv[kRowUnroll];
+        double2* wp[kRowUnroll];
+        double dd[kRowUnroll];
+#pragma unroll
+        for (int u = 0; u < kRowUnroll; ++u) {
+            const int idx = base + u * kApply + ta;
+            wp[u] = nullptr;
+            if (idx < items) {
+                const int e = e_lo + idx / per;
+                if (only < 0 || L_ph[e] == only) {
+                    const int rem = idx - (idx / per) * per;
+                    const int h = rem >= w2;
+                    const int j2 = rem - h * w2;
+                    const int2 rs = L_rs[e];
+                    dd[u] = L_d[e];
+                    const int dst = h ? rs.y : rs.x;
+                    const int src = h ? rs.x : rs.y;
+                    wp[u] = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
+                    tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
+                    wv[u] = __ldcg(wp[u]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRowUnroll; ++u) {
+            if (wp[u]) {
+                wv[u].x = fma(dd[u], tv[u].x, wv[u].x);
+                wv[u].y = fma(dd[u], tv[u].y, wv[u].y);
+                *wp[u] = wv[u];
+            }
+        }
+    }
+}
+
+
+__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+struct Smem {
+    int2* L_rs;     // [kPairCap]  delta-list chunk
+    double* L_d;    // [kPairCap]
+    double* L_new;  // [kPairCap]
+    int* L_ph;      // [kPairCap]
+    int* s_off;     // [kBatch * nblk + 1]
+    unsigned* bm;   // [(p + 31) / 32]
+    double* td;     // [p] T diagonal, or NULL
+    int* cX;        // [cellcap] row of each block cell (-1: phantom)
+    double* cW;     // [cellcap] cell value brought forward to the start of the block
+    double* cO;     // [cellcap] Omega of the cell
+    double* cT;     // [cellcap][kDMax-1] T entries of the block's earlier phases
+    double* sd;     // [kDMax][rmax] delta of each pair of the block's phases (extended ranges)
+    short* cQ;      // [cellcap][kDMax-1] index into sd[i] of the cell row's pair at in-block phase i
+};
+
+__global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_epoch, s_blk, s_stop, s_staged, s_iters, s_conv;
+    __shared__ int s_cnt[2];
+    __shared__ int s_aE, s_aBlk, s_aStop, s_nent, s_multi, s_conflict;
+    __shared__ int s_wsum[kApplyWarps];
+    __shared__ int s_lo[kDMax], s_cb[kDMax + 1], s_slot[kDMax + 1], s_ncell, s_rd0, s_ph0w;
+    __shared__ double s_red[4][kApplyWarps];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = blockIdx.x, bl = b, nblk = gridDim.x;
+    const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half;
+    const int D = a.D, NB = a.NB;
+    const int c0 = b * w;
+    const int wl = max(0, min(w, p - c0));
+    const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
+    double* __restrict__ Wb = a.W + (long long)b * a.slab;
+    const double* __restrict__ Tb = a.T + (long long)b * a.slab;
+    double* __restrict__ Ob = a.Om + (long long)b * a.slab;
+    const int* lcntL = a.list_cnt;
+    const int2* lrsL = a.list_rs;
+    const double2* ldnL = a.list_dn;
+
+    Smem sm;
+    {
+        unsigned char* ptr = smem_raw;
+        auto take = [&](size_t bytes) {
+            unsigned char* r = ptr;
+            ptr += (bytes + 15) & ~(size_t)15;
+            return r;
+        };
+        sm.L_rs = reinterpret_cast<int2*>(take(sizeof(int2) * kPairCap));
+        sm.L_d = reinterpret_cast<double*>(take(sizeof(double) * kPairCap));
+        sm.L_new = reinterpret_cast<double*>(take(sizeof(double) * kPairCap));
+        sm.L_ph = reinterpret_cast<int*>(take(sizeof(int) * kPairCap));
+        sm.s_off = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)kBatch * nblk + 1)));
+        sm.bm = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (size_t)((p + 31) / 32)));
+        sm.cX = reinterpret_cast<int*>(take(sizeof(int) * (size_t)a.cellcap));
+        sm.cW = reinterpret_cast<double*>(take(sizeof(double) * (size_t)a.cellcap));
+        sm.cO = reinterpret_cast<double*>(take(sizeof(double) * (size_t)a.cellcap));
+        sm.cT = reinterpret_cast<double*>(take(sizeof(double) * (size_t)a.cellcap * (kDMax - 1)));
+        sm.sd = reinterpret_cast<double*>(take(sizeof(double) * (size_t)kDMax * a.rmax));
+        sm.cQ = reinterpret_cast<short*>(take(sizeof(short) * (size_t)a.cellcap * (kDMax - 1)));
+        sm.td = a.tdiag_smem ? reinterpret_cast<double*>(take(sizeof(double) * (size_t)p)) : nullptr;
+    }
+    if (sm.td)
+        for (int i = tid; i < p; i += kThreads) sm.td[i] = __ldg(a.tdiag + i);
+    for (int i = tid; i < (p + 31) / 32; i += kThreads) sm.bm[i] = 0u;
+#define TD(i) (sm.td ? sm.td[i] : __ldg(a.tdiag + (i)))
+
+    // ---- stage blocks 0 and 1 from the initial W, Omega (watermark -1)
+    for (int bb = 0; bb < 2 && bb < 2 * NB; ++bb) {
+        const Blk k = block_at(bb, m, D, NB);
+        for (int idx = tid; idx < k.len * wl; idx += kThreads) {
+            const int i = idx / wl, j = idx - i * wl;
+            const int Q = k.g0 + i;
+            const int c = c0 + j;
+            const int x = pub_row(k.ph0 + i, c, m, p);
+            if (x < 0) continue;
+            const size_t so = (size_t)(Q % a.sr) * p + c;
+            a.stW[so] = Wb[(long long)x * w + j];
+            a.stO[so] = Ob[(long long)x * w + j];
+        }
+    }
+    if (tid == 0) {
+        s_epoch = -1;
+        s_blk = -1;
+        s_stop = -1;
+        s_staged = 1;
+        s_cnt[0] = s_cnt[1] = 0;
+        s_conflict = 0;
+    }
+    __syncthreads();
+
+    unsigned long long* prof = (a.prof && b == 0) ? a.prof : nullptr;
+
+    if (warp < kChainWarps) {
+        // ================================================================ chain warps
+        const int tc = tid;
+        bar_chain();
+        if (tc == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
+        if (b == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
+        double smax = 0.0;  // max |delta| of this thread's own pairs over the sweep
+        int snnz = 0;
+        long long t_wait = 0, t_load = 0, t_work = 0;
+        int blk = 0;
+        while (true) {
+            const long long t0 = clock64();
+            const Blk k = block_at(blk, m, D, NB);
+            if (tc == 0) {
+                wait_counter(a.bar, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk);
+                st_vol(&s_epoch, k.g0);  // deltas and lists of every phase < g0 are visible
+                st_vol(&s_blk, blk);
+            }
+            bar_chain();
+            const long long t1 = clock64();
+            t_wait += t1 - t0;
+            // ---- the previous block closed a sweep: convergence decision (identical in every CTA)
+            if (k.ph0 == 0 && blk > 0) {
+                const int it = k.sweep - 1;
+                const double dmax_all =
+                    __longlong_as_double((long long)__ldcg(a.dmax + (a.it_base + it) % WFORM_DMAX_RING));
+                const bool stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter);
+                if (b == 0 && tc == 0) {
+                    a.rec_delta[it] = dmax_all;
+                    a.rec_time[it + 1] = globaltimer_ns();
+                    a.dmax[(a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
+                }
+                if (stop) {
+                    if (tc == 0) {
+                        s_iters = it + 1;
+                        s_conv = dmax_all < a.delta_tol;
+                        __threadfence_block();
+                        st_vol(&s_stop, k.g0 - 1);
+                    }
+                    break;
+                }
+            }
+            const bool has_diag = (k.ph0 + k.len - 1 == m);
+            const int nbc = k.len - (has_diag ? 1 : 0);  // colour phases of the block
+            const int Cp = stage_mark(blk, m, D, NB);
+            // cell layout: colour d = 0..nbc-1 covers pairs [lo_d, hi_d), two cells per pair;
+            // then the diagonal cells (rows of the own pairs at colour m-1)
+            if (tc == 0) {
+                int nc = 0;
+                for (int d = 0; d < kDMax; ++d) {
+                    const int h = nbc - 1 - d;
+                    s_lo[d] = (d < nbc) ? max(0, q_lo - h) : 0;
+                    const int hi = (d < nbc) ? min(half, q_hi + h) : 0;
+                    s_cb[d] = nc;
+                    nc += (d < nbc) ? 2 * (hi - s_lo[d]) : 0;
+                }
+                s_cb[kDMax] = nc;
+                s_ncell = nc;
+                for (int d = 0; d <= kDMax; ++d) s_slot[d] = (k.g0 + d) % a.sr;
+                s_rd0 = (Cp + 1) % a.rd;
+                s_ph0w = (Cp + 1) % (m + 1);
+            }
+            bar_chain();
+            const int ncell = s_ncell;
+            const int ndiag = has_diag ? 2 * (q_hi - q_lo) : 0;
+            const int ntot = ncell + ndiag;
+
+            // ---- cells: stage value, deltas of the two previous blocks, T entries of this block
+            for (int ci = tc; ci < ntot; ci += kChain) {
+                int d, x, c;
+                if (ci < ncell) {
+                    d = 0;
+                    while (d + 1 < nbc && ci >= s_cb[d + 1]) ++d;
+                    const int rel = ci - s_cb[d];
+                    const int q = s_lo[d] + (rel >> 1);
+                    int r, s2;
+                    round_pair(q, m, m - 1 - (k.ph0 + d), r, s2);
+                    if (s2 >= p) {
+                        sm.cX[ci] = -1;
+                        continue;
+                    }
+                    x = (rel & 1) ? s2 : r;
+                    c = (rel & 1) ? r : s2;
+                } else {
+                    d = nbc;
+                    const int rel = ci - ncell;
+                    const int q = q_lo + (rel >> 1);
+                    int r, s2;
+                    round_pair(q, m, 0, r, s2);  // colour m-1
+                    x = (rel & 1) ? s2 : r;
+                    if (x >= p) {
+                        sm.cX[ci] = -1;
+                        continue;
+                    }
+                    c = x;
+                }
+                const int cs = c / w;  // slab of column c
+                const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
+                const size_t so = (size_t)s_slot[d] * p + c;
+                double val = __ldcg(a.stW + so);
+                const double om = __ldcg(a.stO + so);
+                // in-block phases ph0 .. ph0+d-1 (all colours): the row's partner (T entry, loaded
+                // unconditionally) and the row's pair index (into sd), both stepped without division
+                double tin[kDMax - 1];
+                {
+                    int y = circle_partner(x, k.ph0, m);
+                    int pos = (x == 0) ? 0 : 1 + (x - 1 + k.ph0) % m;
+#pragma unroll
+                    for (int i = 0; i < kDMax - 1; ++i) {
+                        tin[i] = 0.0;
+                        if (i < d) {
+                            if (y < p) tin[i] = __ldcg(Tc + (long long)y * w);
+                            const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
+                            sm.cQ[(size_t)ci * (kDMax - 1) + i] = (short)(qi - s_lo[i]);
+                            // step to phase ph0 + i + 1
+                            if (x == 0) {
+                                y = (y == 1) ? m : y - 1;
+                            } else {
+                                int yy = (y == 0) ? x : y;
+                                yy -= 2;
+                                if (yy < 1) yy += m;
+                                y = (yy == x) ? 0 : yy;
+                                pos = (pos == m) ? 1 : pos + 1;
+                            }
+                        }
+                    }
+                }
+                // deltas of the phases Cp+1 .. g0-1 (the two previous blocks), in order
+                {
+                    int slot = s_rd0, phw = s_ph0w;
+                    for (int j0 = Cp + 1; j0 < k.g0; j0 += 8) {
+                        double dj[8];
+                        int phs[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            dj[u] = (j0 + u < k.g0) ? __ldcg(a.dring + (size_t)slot * p + x) : 0.0;
+                            phs[u] = phw;
+                            slot = (slot + 1 == a.rd) ? 0 : slot + 1;
+                            phw = (phw == m) ? 0 : phw + 1;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (dj[u] != 0.0) {
+                                const int y = src_row(phs[u], x, m);
+                                val = fma(dj[u], __ldcg(Tc + (long long)y * w), val);
+                            }
+                        }
+                    }
+                }
+                sm.cX[ci] = x;
+                sm.cW[ci] = val;
+                sm.cO[ci] = om;
+#pragma unroll
+                for (int i = 0; i < kDMax - 1; ++i) sm.cT[(size_t)ci * (kDMax - 1) + i] = tin[i];
+            }
+            bar_chain();
+            const long long t2 = clock64();
+            t_load += t2 - t1;
+
+            // ---- the block's colours, in order, in shared memory
+            for (int d = 0; d < nbc; ++d) {
+                const int ph = k.ph0 + d;
+                const int Q = k.g0 + d;
+                const int h = nbc - 1 - d;
+                const int hi = min(half, q_hi + h);
+                const int lod = s_lo[d], cbd = s_cb[d];
+                const int c1 = m - 1 - ph;
+                const int lslot = Q % a.rl;
+                const size_t dgo = (size_t)(Q % a.rd) * p;  // once per colour
+                const size_t seg_off = ((size_t)lslot * nblk + b) * a.share;
+                double* sdd = sm.sd + (size_t)d * a.rmax;
+                const int sid = kChain - 1 - tc;
+                for (int base = lod; base < hi; base += kChain) {
+                    const int q = base + sid;
+                    int r = 0, s = 0;
+                    double dl = 0.0, nv = 0.0;
+                    const bool own = q >= q_lo && q < q_hi;
+                    if (q < hi) {
+                        round_pair(q, m, c1, r, s);
+                        if (s < p) {
+                            const int ci = cbd + 2 * (q - lod);
+                            double v2[2];
+#pragma unroll
+                            for (int side = 0; side < 2; ++side) {
+                                const int cc = ci + side;
+                                const int x = sm.cX[cc];
+                                double val = sm.cW[cc];
+                                (void)x;
+                                for (int i = 0; i < d; ++i) {
+                                    const double di = sm.sd[(size_t)i * a.rmax + sm.cQ[(size_t)cc * (kDMax - 1) + i]];
+                                    if (di != 0.0) val = fma(di, sm.cT[(size_t)cc * (kDMax - 1) + i], val);
+                                }
+                                v2[side] = val;
+                            }
+                            // side 0: cell (r, s) = W[r,s]; side 1: cell (s, r) = W[s,r]
+                            const double om = sm.cO[ci];
+                            dl = pair_delta(make_double2(v2[1], om), make_double2(v2[0], om), TD(r), TD(s), a.shrink, nv);
+                            if (own) {
+                                a.dring[dgo + r] = dl;
+                                a.dring[dgo + s] = dl;
+                                if (dl != 0.0) {
+                                    smax = fmax(smax, fabs(dl));
+                                    ++snnz;
+                                }
+                            }
+                        } else if (own) {
+                            a.dring[dgo + r] = 0.0;  // partner is the phantom (odd p)
+                        }
+                        sdd[q - lod] = dl;
+                    }
+                    const bool nz = own && dl != 0.0;
+                    const unsigned mask = __ballot_sync(0xffffffffu, nz);
+                    if (mask) {
+                        int basepos = 0;
+                        if (lane == 0) basepos = atomicAdd(&s_cnt[d & 1], __popc(mask));
+                        basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                        if (nz) {
+                            const int at = basepos + __popc(mask & ((1u << lane) - 1u));
+                            a.list_rs[seg_off + at] = make_int2(r, s);
+                            a.list_dn[seg_off + at] = make_double2(dl, nv);
+                        }
+                    }
+                }
+                bar_chain();
+                if (tc == 0) {
+                    a.list_cnt[(size_t)lslot * nblk + b] = s_cnt[d & 1];
+                    s_cnt[d & 1] = 0;
+                }
+            }
+
+            // ---- diagonal phase (closes the sweep): rows of the own pairs at colour m-1
+            if (has_diag) {
+                const int Qd = k.g0 + nbc;
+                const size_t dgo = (size_t)(Qd % a.rd) * p;
+                double dm = 0.0;
+                for (int e = tc; e < ndiag; e += kChain) {
+                    const int cc = ncell + e;
+                    const int x = sm.cX[cc];
+                    if (x < 0) continue;
+                    double val = sm.cW[cc];
+                    for (int i = 0; i < nbc; ++i) {
+                        const double di = sm.sd[(size_t)i * a.rmax + sm.cQ[(size_t)cc * (kDMax - 1) + i]];
+                        if (di != 0.0) val = fma(di, sm.cT[(size_t)cc * (kDMax - 1) + i], val);
+                    }
+                    const double om = sm.cO[cc];
+                    const double nv = diag_from_dot(val, om, TD(x), a.n);
+                    const double dl = __dsub_rn(nv, om);
+                    a.dring[dgo + x] = dl;
+                    a.diagv[x] = make_double2(dl, nv);
+                    dm = fmax(dm, fabs(dl));
+                }
+                // this sweep's statistics: off-diagonal (own pairs) and diagonal maxima, non-zero count
+                const double mw = warp_max(fmax(dm, smax));
+                const double nw = warp_sum((double)snnz);
+                if (lane == 0) {
+                    s_red[0][warp] = mw;
+                    s_red[1][warp] = nw;
+                }
+                smax = 0.0;
+                snnz = 0;
+                bar_chain();
+                if (tc == 0) {
+                    double mb = 0.0, nbk = 0.0;
+                    for (int j = 0; j < kChainWarps; ++j) {
+                        mb = fmax(mb, s_red[0][j]);
+                        nbk += s_red[1][j];
+                    }
+                    atomicMax(a.dmax + (a.it_base + k.sweep) % WFORM_DMAX_RING, (unsigned long long)__double_as_longlong(mb));
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + k.sweep), (unsigned long long)nbk);
+                }
+            }
+            t_work += clock64() - t2;
+            // ---- the next block's cells must be staged (by this CTA's apply warps) before arriving
+            if (tc == 0) {
+                while (ld_acquire_cta(&s_staged) < blk + 1) {
+                }
+                asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
+            }
+            ++blk;
+        }
+        if (prof && tc == 0) {
+            prof[0] = (unsigned long long)t_wait;
+            prof[1] = (unsigned long long)t_load;
+            prof[2] = (unsigned long long)t_work;
+            prof[3] = (unsigned long long)blk;
+        }
+    } else {
+        // ================================================================ apply warps
+        const int ta = tid - kChain;
+        int C = -1;    // every phase <= C is in the own slab
+        int cph = m;   // phase-in-sweep of C
+        int cit = -1;  // sweep of C
+        int staged = 1;  // highest block staged
+        long long t_busy = 0, t_idle = 0, nbatch = 0, t_diag = 0, t_stage = 0;
+        while (true) {
+            const long long t0 = clock64();
+            bar_apply();
+            if (ta == 0) {
+                s_aE = ld_vol(&s_epoch);
+                s_aBlk = ld_vol(&s_blk);
+                s_aStop = ld_vol(&s_stop);
+                s_nent = 0;
+                s_multi = 0;
+                s_conflict = 0;
+                __threadfence_block();
+            }
+            bar_apply();
+            const int E = s_aE;
+            const int cblk = s_aBlk;
+            const int stopg = s_aStop;
+            const int avail = (stopg >= 0) ? stopg : E - 1;
+            const int k0 = C + 1;
+            const int ph0 = (cph == m) ? 0 : cph + 1;
+            const int it0 = (cph == m) ? cit + 1 : cit;
+            const bool have = C < avail;
+            const bool diag = have && ph0 == m;
+            const int k1 = (have && !diag) ? min(min(avail, k0 + kBatch - 1), k0 + (m - 1 - ph0)) : C;
+            const int nb = k1 - C;
+            const int nsh = nblk;
+            const int nseg = nb * nsh;
+            // next block to stage: the chain at block cblk needs block cblk+1 before arriving;
+            // stage up to cblk+2.  Its watermark C' must be <= E-1 (deltas known) and the
+            // window (C, C'] must still be in the delta ring.
+            const int sb = staged + 1;
+            const int Cp = stage_mark(sb, m, D, NB);
+            const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 2 && Cp <= E - 1 && C >= Cp - a.stage_window;
+            if (!have && !can_stage) {
+                t_idle += clock64() - t0;
+                __nanosleep(32);
+                continue;
+            }
+
+            // ---- segment heads (count + first entry) of the batch's colours
+            for (int idx = ta; idx < nseg; idx += kApply) {
+                const int jb = idx / nsh;
+                const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
+                const int cnt = __ldcg(lcntL + seg);
+                const int2 rs = __ldcg(lrsL + (size_t)seg * a.share);
+                const double2 dn = __ldcg(ldnL + (size_t)seg * a.share);
+                sm.s_off[idx] = cnt;
+                if (cnt > 1) s_multi = 1;
+                if (cnt == 1) {
+                    const int pos = atomicAdd(&s_nent, 1);
+                    if (pos < kPairCap) {
+                        sm.L_rs[pos] = rs;
+                        sm.L_d[pos] = dn.x;
+                        sm.L_ph[pos] = jb;
+                    } else {
+                        s_multi = 1;
+                    }
+                    if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
+                    if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                }
+            }
+            // ---- stage block sb: cells brought forward from this slab's watermark C to C'
+            if (can_stage) {
+                const long long ts = clock64();
+                const Blk kb = block_at(sb, m, D, NB);
+                for (int idx = ta; idx < kb.len * wl; idx += kApply) {
+                    const int i = idx / wl, j = idx - i * wl;
+                    const int Q = kb.g0 + i;
+                    const int c = c0 + j;
+                    const int x = pub_row(kb.ph0 + i, c, m, p);
+                    if (x < 0) continue;
+                    double val = __ldcg(Wb + (long long)x * w + j);
+                    const double om = __ldcg(Ob + (long long)x * w + j);
+                    for (int j0 = C + 1; j0 <= Cp; j0 += 8) {
+                        double dj[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            dj[u] = (j0 + u <= Cp) ? __ldcg(a.dring + (size_t)((j0 + u) % a.rd) * p + x) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (dj[u] != 0.0) {
+                                const int y = src_row((j0 + u) % (m + 1), x, m);
+                                val = fma(dj[u], __ldcg(Tb + (long long)y * w + j), val);
+                            }
+                        }
+                    }
+                    const size_t so = (size_t)(Q % a.sr) * p + c;
+                    a.stW[so] = val;
+                    a.stO[so] = om;
+                }
+                t_stage += clock64() - ts;
+            }
+            bar_apply();
+            if (can_stage) {
+                staged = sb;
+                if (ta == 0) {
+                    __threadfence_block();
+                    st_vol(&s_staged, staged);
+                }
+            }
+
+            if (diag) {
+                // ---- dense diagonal step over the own slab (+ objective records)
+                const double2* dd = a.diagv;
+                double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
+                for (int i0 = 0; i0 < p; i0 += kPairCap) {
+                    const int iend = min(i0 + kPairCap, p);
+                    for (int i = i0 + ta; i < iend; i += kApply) {
+                        const double2 v = ldcg2(dd + i);
+                        sm.L_d[i - i0] = v.x;
+                        sm.L_new[i - i0] = v.y;
+                    }
+                    bar_apply();
+                    const int items = (iend - i0) * w2;
+                    for (int base = 0; base < items; base += kApply * kUnroll) {
+                        double2 wv[kUnroll], tv[kUnroll], ov[kUnroll];
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int idx = base + u * kApply + ta;
+                            if (idx < items) {
+                                const int ii = idx / w2;
+                                const int j2 = idx - ii * w2;
+                                const long long off = (long long)(i0 + ii) * w + 2 * j2;
+                                wv[u] = __ldcg(reinterpret_cast<const double2*>(Wb + off));
+                                if (sm.L_d[ii] != 0.0) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + off));
+                                if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int idx = base + u * kApply + ta;
+                            if (idx < items) {
+                                const int ii = idx / w2;
+                                const int j2 = idx - ii * w2;
+                                const int i = i0 + ii;
+                                const long long off = (long long)i * w + 2 * j2;
+                                const double d = sm.L_d[ii];
+                                if (d != 0.0) {
+                                    wv[u].x = fma(d, tv[u].x, wv[u].x);
+                                    wv[u].y = fma(d, tv[u].y, wv[u].y);
+                                    *reinterpret_cast<double2*>(Wb + off) = wv[u];
+                                }
+                                const int cj = c0 + 2 * j2;
+                                const bool dg0 = (cj == i), dg1 = (cj + 1 == i);
+                                if (a.want_trace) {
+                                    if (dg0 | dg1) {
+                                        if (dg0) ov[u].x = sm.L_new[ii];
+                                        if (dg1) ov[u].y = sm.L_new[ii];
+                                        *reinterpret_cast<double2*>(Ob + off) = ov[u];
+                                        log_acc += log(sm.L_new[ii]);
+                                    }
+                                    q_acc = fma(wv[u].x, ov[u].x, q_acc);
+                                    q_acc = fma(wv[u].y, ov[u].y, q_acc);
+                                    if (i < cj) pen_acc += fabs(ov[u].x);
+                                    if (i < cj + 1) pen_acc += fabs(ov[u].y);
+                                } else if (dg0 | dg1) {
+                                    Ob[off + (dg0 ? 0 : 1)] = sm.L_new[ii];
+                                }
+                            }
+                        }
+                    }
+                    bar_apply();
+                }
+                if (a.want_trace) {
+                    q_acc = warp_sum(q_acc);
+                    pen_acc = warp_sum(pen_acc);
+                    log_acc = warp_sum(log_acc);
+                    const int wa = ta >> 5;
+                    if (lane == 0) {
+                        s_red[1][wa] = q_acc;
+                        s_red[2][wa] = pen_acc;
+                        s_red[3][wa] = log_acc;
+                    }
+                    bar_apply();
+                    if (ta == 0) {
+                        double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                        for (int j = 0; j < kApplyWarps; ++j) {
+                            v1 += s_red[1][j];
+                            v2 += s_red[2][j];
+                            v3 += s_red[3][j];
+                        }
+                        double* ro = a.rec_obj + ((size_t)it0 * gridDim.x + bl) * 3;
+                        ro[0] = v1;
+                        ro[1] = v2;
+                        ro[2] = v3;
+                    }
+                }
+                C = k0;
+                cph = m;
+                cit = it0;
+                t_diag += clock64() - t0;
+            } else if (nb > 0) {
+                // ---- colour phases k0 .. k1
+                int total = 0;
+                if (!s_multi) {
+                    // every segment had at most one entry: they are already in shared memory
+                    const int nent = s_nent;
+                    if (nb > 1) {
+                        for (int e = ta; e < nent; e += kApply) {
+                            const int2 rs = sm.L_rs[e];
+                            const unsigned br = 1u << (rs.x & 31), bs = 1u << (rs.y & 31);
+                            const unsigned o1 = atomicOr(sm.bm + (rs.x >> 5), br);
+                            const unsigned o2 = atomicOr(sm.bm + (rs.y >> 5), bs);
+                            if ((o1 & br) | (o2 & bs)) s_conflict = 1;
+                        }
+                        bar_apply();
+                    }
+                    if (!s_conflict) {
+                        apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, nent, w2, Wb, Tb, ta);
+                    } else {
+                        for (int jb = 0; jb < nb; ++jb) {  // rows repeat across phases: phase by phase
+                            apply_rows(sm.L_rs, sm.L_d, sm.L_ph, jb, 0, nent, w2, Wb, Tb, ta);
+                            bar_apply();
+                        }
+                    }
+                    bar_apply();
+                    if (nb > 1) {
+                        for (int e = ta; e < nent; e += kApply) {
+                            const int2 rs = sm.L_rs[e];
+                            atomicAnd(sm.bm + (rs.x >> 5), ~(1u << (rs.x & 31)));
+                            atomicAnd(sm.bm + (rs.y >> 5), ~(1u << (rs.y & 31)));
+                        }
+                    }
+                    total = nent;
+                } else {
+                    // general path: exclusive scan of the segment counts, entries in phase order
+                    total = apply_scan(sm.s_off, nseg, ta, s_wsum);
+                    for (int e0 = 0; e0 < total; e0 += kPairCap) {
+                        const int e1 = min(total, e0 + kPairCap);
+                        for (int e = e0 + ta; e < e1; e += kApply) {
+                            int lo = 0, hi = nseg;  // segment: s_off[lo] <= e < s_off[lo+1]
+                            while (hi - lo > 1) {
+                                const int mid = (lo + hi) >> 1;
+                                if (sm.s_off[mid] <= e) lo = mid;
+                                else hi = mid;
+                            }
+                            const int jb = lo / nsh;
+                            const int rank = e - sm.s_off[lo];
+                            const size_t at =
+                                ((size_t)((k0 + jb) % a.rl) * nblk + (lo - jb * nsh)) * a.share + rank;
+                            const int2 rs = __ldcg(lrsL + at);
+                            const double2 dn = __ldcg(ldnL + at);
+                            // segments with one entry had their Omega cells written above
+                            if (sm.s_off[lo + 1] - sm.s_off[lo] > 1) {
+                                if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
+                                if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                            }
+                            sm.L_rs[e - e0] = rs;
+                            sm.L_d[e - e0] = dn.x;
+                            sm.L_ph[e - e0] = jb;
+                            if (nb > 1) {
+                                const unsigned br = 1u << (rs.x & 31), bs = 1u << (rs.y & 31);
+                                const unsigned o1 = atomicOr(sm.bm + (rs.x >> 5), br);
+                                const unsigned o2 = atomicOr(sm.bm + (rs.y >> 5), bs);
+                                if ((o1 & br) | (o2 & bs)) s_conflict = 1;
+                            }
+                        }
+                        bar_apply();
+                        const int conflict = s_conflict;
+                        if (!conflict) {
+                            apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, e1 - e0, w2, Wb, Tb, ta);
+                        } else {
+                            for (int jb = 0; jb < nb; ++jb) {
+                                const int lo = max(sm.s_off[jb * nsh], e0) - e0;
+                                const int hi = min(sm.s_off[(jb + 1) * nsh], e1) - e0;
+                                if (lo < hi) apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, lo, hi, w2, Wb, Tb, ta);
+                                bar_apply();
+                            }
+                        }
+                        bar_apply();
+                        if (nb > 1) {
+                            for (int e = ta; e < e1 - e0; e += kApply) {
+                                const int2 rs = sm.L_rs[e];
+                                atomicAnd(sm.bm + (rs.x >> 5), ~(1u << (rs.x & 31)));
+                                atomicAnd(sm.bm + (rs.y >> 5), ~(1u << (rs.y & 31)));
+                            }
+                        }
+                        bar_apply();
+                        if (ta == 0) s_conflict = 0;
+                    }
+                }
+                C = k1;
+                cph = ph0 + (k1 - k0);
+                cit = it0;
+                ++nbatch;
+            }
+            t_busy += clock64() - t0;
+            if (stopg >= 0 && C >= stopg) break;
+        }
+        if (prof && ta == 0) {
+            prof[4] = (unsigned long long)t_busy;
+            prof[5] = (unsigned long long)t_idle;
+            prof[6] = (unsigned long long)nbatch;
+            prof[10] = (unsigned long long)t_stage;
+            prof[11] = (unsigned long long)t_diag;
+        }
+    }
+#undef TD
+    __syncthreads();
+    if (b == 0 && tid == 0) {
+        a.status[0] = s_iters;
+        a.status[1] = s_conv;
+    }
+}
+
+}  // namespace qb
+
+int qblock_cellcap(int share, int D) { return 2 * D * (share + 2 * (D - 1)) + 2 * share + 8; }
+
+int qblock_rmax(int share, int D) { return share + 2 * (D - 1) + 2; }
+
+size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem) {
+    auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    const size_t cap = (size_t)qblock_cellcap(share, D);
+    size_t b = 0;
+    b += al(sizeof(int2) * qb::kPairCap) + 2 * al(sizeof(double) * qb::kPairCap) + al(sizeof(int) * qb::kPairCap);
+    b += al(sizeof(int) * ((size_t)qb::kBatch * nblk + 1));
+    b += al(sizeof(unsigned) * (size_t)((p + 31) / 32));
+    b += al(sizeof(int) * cap) + 2 * al(sizeof(double) * cap) + al(sizeof(double) * cap * (qb::kDMax - 1));
+    b += al(sizeof(double) * (size_t)qb::kDMax * qblock_rmax(share, D));
+    b += al(sizeof(short) * cap * (qb::kDMax - 1));
+    if (tdiag_smem) b += al(sizeof(double) * (size_t)p);
+    return b;
+}
+
+cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
+    const size_t smem = qblock_smem_bytes(args.p, nblk, args.share, args.D, args.tdiag_smem);
+    cudaError_t e = cudaFuncSetAttribute(qb::pcd_qblock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    QbArgs copy = args;
+    void* kargs[] = {&copy};
+    return cudaLaunchCooperativeKernel((void*)qb::pcd_qblock_kernel, dim3(nblk), dim3(qb::kThreads), kargs, smem, st);
+}
+
+}  // namespace concord

@@ -81,6 +81,59 @@ struct WformArgs {
     unsigned long long* prof;       // optional [16] cycle counters (CTA 0), or NULL
 };
 
+// Temporally blocked variant (pcd_qblock.cu): D colour phases per grid barrier.
+#ifndef QB_DMAX
+#define QB_DMAX 8
+#endif
+#ifndef QB_DEFAULT
+#define QB_DEFAULT 0        // 1: single-device solvers use the temporally blocked kernel by default
+#endif
+#ifndef QB_CHAIN_WARPS
+#define QB_CHAIN_WARPS 8     // chain warps of the blocked kernel (the block's cells are loaded in parallel)
+#endif
+#ifndef QB_DEFAULT_D
+#define QB_DEFAULT_D 4
+#endif
+struct QbArgs {
+    int p, m, half, w;
+    long long slab;
+    double* W;
+    const double* T;
+    double* Om;
+    const double* tdiag;
+    int tdiag_smem;
+    double2* diagv;        // [p] (delta, new) of the latest diagonal step
+    double* stW;           // [sr][p] staged cell values (W at the block's stage watermark)
+    double* stO;           // [sr][p] staged Omega of the cells
+    int sr;                // stage slots (phases)
+    double* dring;         // [rd][p] per-row delta of each recent phase
+    int rd;
+    int2* list_rs;         // [rl][nblk][share]
+    double2* list_dn;
+    int* list_cnt;         // [rl][nblk]
+    int rl;
+    int share;
+    unsigned long long* bar;
+    unsigned long long* dmax;  // [WFORM_DMAX_RING]
+    unsigned long long bar_base;
+    int it_base;
+    double n, shrink, delta_tol;
+    int max_iter, want_trace;
+    int D, NB;             // phases per block, blocks per sweep
+    int cellcap, rmax;     // shared-memory sizing of the block cells
+    int stage_window;      // max phases a stage may be brought forward over
+    double* rec_delta;
+    double* rec_obj;       // [max_iter][nblk][3]
+    unsigned long long* rec_time;
+    long long* rec_nnz;
+    int* status;
+    unsigned long long* prof;
+};
+int qblock_cellcap(int share, int D);
+int qblock_rmax(int share, int D);
+size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem);
+cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st);
+
 // Lag cap for a slab width (bounded by the stage ring's shared memory) and m.
 int wform_lag_cap(int w, int m);
 int wform_tdiag_in_smem(int p);
