@@ -59,7 +59,8 @@ typedef struct {
     int64_t col0;             /* first column this solver holds                             */
     int64_t ncols;            /* columns this solver holds (p unless it is one shard)       */
     int32_t lag_cap;          /* phases the apply warps may trail the colour chain          */
-    int32_t reserved;
+    int32_t kernel;           /* 0: per-phase chain (pcd_wform_kernel), D >= 1: temporally   */
+                              /*    blocked chain with D colours per barrier (pcd_qblock)    */
 } concord_layout;
 
 typedef struct {

@@ -75,7 +75,7 @@ class Layout(ctypes.Structure):
         ("col0", ctypes.c_int64),
         ("ncols", ctypes.c_int64),
         ("lag_cap", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("kernel", ctypes.c_int32),
     ]
 
 

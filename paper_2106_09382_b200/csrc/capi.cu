@@ -484,6 +484,7 @@ int concord_solver_layout(concord_solver* s, concord_layout* out) {
     out->col0 = s->blk0 * s->w < s->p ? s->blk0 * s->w : s->p;
     out->ncols = ncols_local(s);
     out->lag_cap = s->lmax;
+    out->kernel = s->qb ? s->qb_D : 0;
     return CONCORD_OK;
 }
 

@@ -86,10 +86,10 @@ struct WformArgs {
 #define QB_DMAX 8
 #endif
 #ifndef QB_DEFAULT
-#define QB_DEFAULT 0        // 1: single-device solvers use the temporally blocked kernel by default
+#define QB_DEFAULT 1        // 1: single-device solvers use the temporally blocked kernel by default
 #endif
 #ifndef QB_CHAIN_WARPS
-#define QB_CHAIN_WARPS 8     // chain warps of the blocked kernel (the block's cells are loaded in parallel)
+#define QB_CHAIN_WARPS 6     // chain warps of the blocked kernel (the block's cells are loaded in parallel)
 #endif
 #ifndef QB_DEFAULT_D
 #define QB_DEFAULT_D 4

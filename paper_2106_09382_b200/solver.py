@@ -193,7 +193,7 @@ class Solver:
         """Column partition: slab width, shards, CTAs, this solver's column range."""
         lay = _lib.Layout()
         _lib.check(_lib.load().concord_solver_layout(self._h, ctypes.byref(lay)))
-        return {f: getattr(lay, f) for f, _ in _lib.Layout._fields_ if f != "reserved"}
+        return {f: getattr(lay, f) for f, _ in _lib.Layout._fields_}
 
     def set_stream(self, stream_ptr):
         _lib.check(_lib.load().concord_solver_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))
