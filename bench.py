@@ -14,7 +14,7 @@ lambda reported beside it.
   HBM; the W/T/Omega working set (3 x 200 MB) exceeds the 126 MB L2.
 * e2e: the same metric through the public API `pcd_fit(GramMatrix, SolverConfig)`
   with T in pinned host memory: every step uploads T (H2D) and reads Omega back (D2H).
-* roofline: pcd_wform_kernel's algorithmic bytes per launch / its event time.
+* roofline: the fit kernel's (pcd_qblock_kernel, or pcd_wform_kernel) algorithmic bytes per launch / its event time.
 * cpu_baseline / --impl reference: the reference's own compiled sweep
   (oracle/_ref, built from /root/reference's _ckernels.pyx) on all host cores,
   timed on a bounded sample of rounds (sweep cost is data-independent).
@@ -290,7 +290,7 @@ def run_ours(args, d):
     sweeps = d.sum(sum(f[1] for f in fits))
     value = sweeps / (elapsed_ms / 1e3)
 
-    # roofline of the dominant kernel (pcd_wform_kernel), per launch
+    # roofline of the dominant kernel (the fit kernel), per launch
     kern_ms = [f[2] for f in fits]
     bytes_per = [algorithmic_bytes(p, f[3]) for f in fits]
     avg_ms = sum(kern_ms) / len(kern_ms)

@@ -110,6 +110,7 @@ struct concord_solver {
     int qb_D = 0, qb_NB = 0, qb_sr = 0, qb_rd = 0, qb_rl = 0;
     double* qb_stW = nullptr;
     double* qb_stO = nullptr;
+    double* qb_stT = nullptr;
     double2* qb_diagv = nullptr;
     double* qb_dring = nullptr;
     int2* qb_lrs = nullptr;
@@ -298,6 +299,7 @@ int setup_qblock(concord_solver* s) {
     s->qb_rl = 10 * D + 8;
     CK(dalloc(&s->qb_stW, (size_t)s->qb_sr * p));
     CK(dalloc(&s->qb_stO, (size_t)s->qb_sr * p));
+    CK(dalloc(&s->qb_stT, (size_t)s->qb_sr * (QB_DMAX - 1) * p));
     CK(dalloc(&s->qb_diagv, p));
     CK(dalloc(&s->qb_dring, (size_t)s->qb_rd * p));
     CK(dalloc(&s->qb_lrs, (size_t)s->qb_rl * s->nblk_tot * s->share));
@@ -500,6 +502,7 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->diagd);
     cudaFree(s->qb_stW);
     cudaFree(s->qb_stO);
+    cudaFree(s->qb_stT);
     cudaFree(s->qb_diagv);
     cudaFree(s->qb_dring);
     cudaFree(s->qb_lrs);
@@ -660,6 +663,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.diagv = s->qb_diagv;
         q.stW = s->qb_stW;
         q.stO = s->qb_stO;
+        q.stT = s->qb_stT;
         q.sr = s->qb_sr;
         q.dring = s->qb_dring;
         q.rd = s->qb_rd;

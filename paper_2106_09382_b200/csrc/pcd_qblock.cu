@@ -251,6 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const size_t so = (size_t)(Q % a.sr) * p + c;
             a.stW[so] = Wb[(long long)x * w + j];
             a.stO[so] = Ob[(long long)x * w + j];
+            for (int ii = 0; ii < i; ++ii) {
+                const int y = src_row(k.ph0 + ii, x, m);
+                a.stT[((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = (y < p) ? Tb[(long long)y * w + j] : 0.0;
+            }
         }
     }
     if (tid == 0) {
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         if (b == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
         double smax = 0.0;  // max |delta| of this thread's own pairs over the sweep
         int snnz = 0;
-        long long t_wait = 0, t_load = 0, t_work = 0;
+        long long t_wait = 0, t_load = 0, t_work = 0, t_c0 = 0, t_c1 = 0, t_c2 = 0, t_c3 = 0;
         int blk = 0;
         while (true) {
             const long long t0 = clock64();
@@ -361,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     }
                     c = x;
                 }
+                const long long tq0 = clock64();
                 const int cs = c / w;  // slab of column c
                 const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
                 const size_t so = (size_t)s_slot[d] * p + c;
@@ -368,58 +373,68 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const double om = __ldcg(a.stO + so);
                 // in-block phases ph0 .. ph0+d-1 (all colours): the row's partner (T entry, loaded
                 // unconditionally) and the row's pair index (into sd), both stepped without division
+                // in-block phases ph0 .. ph0+d-1 (all colours): T entries staged by the slab owner;
+                // the row's pair index (into sd) stepped without division
                 double tin[kDMax - 1];
-                {
-                    int y = circle_partner(x, k.ph0, m);
-                    int pos = (x == 0) ? 0 : 1 + (x - 1 + k.ph0) % m;
 #pragma unroll
-                    for (int i = 0; i < kDMax - 1; ++i) {
-                        tin[i] = 0.0;
-                        if (i < d) {
-                            if (y < p) tin[i] = __ldcg(Tc + (long long)y * w);
-                            const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
-                            sm.cQ[(size_t)ci * (kDMax - 1) + i] = (short)(qi - s_lo[i]);
-                            // step to phase ph0 + i + 1
-                            if (x == 0) {
-                                y = (y == 1) ? m : y - 1;
-                            } else {
-                                int yy = (y == 0) ? x : y;
-                                yy -= 2;
-                                if (yy < 1) yy += m;
-                                y = (yy == x) ? 0 : yy;
-                                pos = (pos == m) ? 1 : pos + 1;
-                            }
-                        }
+                for (int i = 0; i < kDMax - 1; ++i)
+                    tin[i] = (i < d) ? __ldcg(a.stT + ((size_t)s_slot[d] * (kDMax - 1) + i) * p + c) : 0.0;
+                {
+                    int pos = (x == 0) ? 0 : 1 + (x - 1 + k.ph0) % m;
+                    for (int i = 0; i < d; ++i) {
+                        const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
+                        sm.cQ[(size_t)ci * (kDMax - 1) + i] = (short)(qi - s_lo[i]);
+                        if (x != 0) pos = (pos == m) ? 1 : pos + 1;
                     }
                 }
-                // deltas of the phases Cp+1 .. g0-1 (the two previous blocks), in order
+                const long long tq1 = clock64();
+                // deltas of the phases Cp+1 .. g0-1 (the two previous blocks): which moved row x?
+                // The (rare) corrections themselves need T entries from HBM: they are applied in a
+                // second pass over the flagged cells, all in parallel.
+                // all delta loads first (predicated, back to back); then, for the phases that moved
+                // row x, the T entries (HBM), again back to back; then the FMAs in phase order
                 {
-                    int slot = s_rd0, phw = s_ph0w;
-                    for (int j0 = Cp + 1; j0 < k.g0; j0 += 8) {
-                        double dj[8];
-                        int phs[8];
+                    double dj[2 * kDMax];
+                    int slot = s_rd0;
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            dj[u] = (j0 + u < k.g0) ? __ldcg(a.dring + (size_t)slot * p + x) : 0.0;
-                            phs[u] = phw;
-                            slot = (slot + 1 == a.rd) ? 0 : slot + 1;
+                    for (int u = 0; u < 2 * kDMax; ++u) {
+                        const bool in = Cp + 1 + u < k.g0;
+                        dj[u] = in ? __ldcg(a.dring + (size_t)slot * p + x) : 0.0;
+                        slot = (slot + 1 == a.rd) ? 0 : slot + 1;
+                    }
+                    unsigned mask = 0u;
+#pragma unroll
+                    for (int u = 0; u < 2 * kDMax; ++u)
+                        if (dj[u] != 0.0) mask |= 1u << u;
+                    if (mask) {
+                        double tj[2 * kDMax];
+                        int phw = s_ph0w;
+#pragma unroll
+                        for (int u = 0; u < 2 * kDMax; ++u) {
+                            const bool on = (mask & (1u << u)) != 0;
+                            const int y = on ? src_row(phw, x, m) : x;
+                            tj[u] = on ? __ldcg(Tc + (long long)y * w) : 0.0;
                             phw = (phw == m) ? 0 : phw + 1;
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            if (dj[u] != 0.0) {
-                                const int y = src_row(phs[u], x, m);
-                                val = fma(dj[u], __ldcg(Tc + (long long)y * w), val);
-                            }
-                        }
+                        for (int u = 0; u < 2 * kDMax; ++u)
+                            if (mask & (1u << u)) val = fma(dj[u], tj[u], val);
                     }
                 }
+                const long long tq2 = clock64();
                 sm.cX[ci] = x;
                 sm.cW[ci] = val;
                 sm.cO[ci] = om;
 #pragma unroll
                 for (int i = 0; i < kDMax - 1; ++i) sm.cT[(size_t)ci * (kDMax - 1) + i] = tin[i];
+                if (tc == 0) {
+                    const long long tq3 = clock64();
+                    t_c0 += tq1 - tq0;
+                    t_c1 += tq2 - tq1;
+                    t_c2 += tq3 - tq2;
+                }
             }
+            bar_chain();
             bar_chain();
             const long long t2 = clock64();
             t_load += t2 - t1;
@@ -539,8 +554,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             t_work += clock64() - t2;
             // ---- the next block's cells must be staged (by this CTA's apply warps) before arriving
             if (tc == 0) {
+                const long long tw0 = clock64();
                 while (ld_acquire_cta(&s_staged) < blk + 1) {
                 }
+                t_c3 += clock64() - tw0;
                 asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
             }
             ++blk;
@@ -550,6 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             prof[1] = (unsigned long long)t_load;
             prof[2] = (unsigned long long)t_work;
             prof[3] = (unsigned long long)blk;
+            prof[7] = (unsigned long long)t_c0;
+            prof[8] = (unsigned long long)t_c1;
+            prof[9] = (unsigned long long)t_c3;
         }
     } else {
         // ================================================================ apply warps
@@ -647,6 +667,19 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const size_t so = (size_t)(Q % a.sr) * p + c;
                     a.stW[so] = val;
                     a.stO[so] = om;
+                    // T entries of the block's earlier phases (kb.ph0 .. ph-1), for the chain's in-block FMAs
+                    int y = circle_partner(x, kb.ph0, m);
+                    for (int ii = 0; ii < i; ++ii) {
+                        a.stT[((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = (y < p) ? __ldcg(Tb + (long long)y * w + j) : 0.0;
+                        if (x == 0) {
+                            y = (y == 1) ? m : y - 1;
+                        } else {
+                            int yy = (y == 0) ? x : y;
+                            yy -= 2;
+                            if (yy < 1) yy += m;
+                            y = (yy == x) ? 0 : yy;
+                        }
+                    }
                 }
                 t_stage += clock64() - ts;
             }

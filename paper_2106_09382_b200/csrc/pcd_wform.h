@@ -105,6 +105,7 @@ struct QbArgs {
     double2* diagv;        // [p] (delta, new) of the latest diagonal step
     double* stW;           // [sr][p] staged cell values (W at the block's stage watermark)
     double* stO;           // [sr][p] staged Omega of the cells
+    double* stT;           // [sr][QB_DMAX-1][p] staged T entries of the earlier phases of the cell's block
     int sr;                // stage slots (phases)
     double* dring;         // [rd][p] per-row delta of each recent phase
     int rd;

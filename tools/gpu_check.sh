@@ -16,5 +16,5 @@ timeout 900 python bench.py > gpurun_out/bench.log 2>&1
 echo "bench rc=$?" >> gpurun_out/status.txt
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_fit.py --p 5000 --n 2000 --fits 1 > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/status.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:pcd_wform -c 1 -o gpurun_out/prof_wform python tools/profile_fit.py --p 5000 --n 2000 --fits 1 > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pcd_ -c 1 -o gpurun_out/prof_wform python tools/profile_fit.py --p 5000 --n 2000 --fits 1 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/status.txt

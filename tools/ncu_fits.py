@@ -1,6 +1,6 @@
 """Fit the bench's lambda path once (for ncu; not a bench number).
 
-    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:pcd_wform \
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:pcd_ \
         --csv --log-file gpurun_out/traffic.csv python tools/ncu_fits.py [--p 5000] [--lams 0.55,...]
 """
 import argparse
