@@ -754,12 +754,24 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
                                  "chain:  bar+fence+arrive", "chain:  share (last thread)", "apply:  heads+stage",
                                  "apply:  diagonal steps", "apply:   broadcast bars", "apply:   heads loop (ta0)",
                                  "apply:   stage loop (ta0)"};
+        const char* qnames[15] = {"chain: barrier wait", "chain: cells part B", "chain: colours+diag", "-",
+                                  "apply: busy", "apply: idle", "apply: batches", "chain:  cells part A (prefetch group)",
+                                  "apply:  heads+stage (batches)", "chain:  wait for own stager",
+                                  "apply:  stage", "apply:  diagonal steps", "chain:  colour corrections (q0)",
+                                  "chain:  colour closed form (q0)", "chain:  colour publish (q0)"};
+        if (s->qb) {
+            fprintf(stderr, "  (blocked kernel: per-block figures; %d colours per block)\n", s->qb_D);
+            for (int i = 0; i < 15; ++i) names[i] = qnames[i];
+        }
         for (int i = 0; i < 15; ++i) {
-            if (i == 3 || i == 6) continue;
+            if (i == 3 || i == 6 || names[i][0] == '-') continue;
             const double us = pc[i] / (clk_khz * 1e-3);
             fprintf(stderr, "  %-30s %12.1f us total  %9.3f us/phase\n", names[i], us, us / (ph > 0 ? ph : 1));
         }
         fprintf(stderr, "  %-30s %12llu (%.2f phases/batch)\n", names[6], pc[6], pc[6] ? ph / pc[6] : 0.0);
+        if (s->qb)
+            fprintf(stderr, "  %-30s %12.1f us total  %9.3f us/phase\n", "apply:  rows (batches)", pc[15] / (clk_khz * 1e-3),
+                    pc[15] / (clk_khz * 1e-3) / (ph > 0 ? ph : 1));
     }
     float setup_ms = 0.f, kernel_ms = 0.f;
     CK(cudaEventElapsedTime(&setup_ms, s->ev[0], s->ev[1]));

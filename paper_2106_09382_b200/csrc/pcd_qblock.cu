@@ -50,6 +50,8 @@ constexpr int kBatch = WFORM_BATCH;
 constexpr int kUnroll = 2;
 constexpr int kRowUnroll = 2;
 constexpr int kDMax = QB_DMAX;
+constexpr int kAsyncStages = QB_ASYNC_STAGES;
+constexpr int kChainN = 32;   // batches with row conflicts up to this many entries: per-row chains
 
 __device__ __forceinline__ void bar_chain() { asm volatile("bar.sync 1, %0;" ::"n"(kChain) : "memory"); }
 __device__ __forceinline__ void bar_apply() { asm volatile("bar.sync 2, %0;" ::"n"(kApply) : "memory"); }
@@ -58,6 +60,54 @@ __device__ __forceinline__ void st_vol(int* p, int v) { *reinterpret_cast<volati
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
     int v;
     asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+
+// Clock read that cannot issue before `dep` is available (profiling only).
+__device__ __forceinline__ long long clock_after(double dep) {
+    long long t;
+    asm volatile(
+        "{\n .reg .pred pp;\n setp.eq.f64 pp, %1, 0d7FF0000000000001;\n @pp mov.u64 %0, 0;\n"
+        " @!pp mov.u64 %0, %%clock64;\n}"
+        : "=l"(t)
+        : "d"(dep)
+        : "memory");
+    return t;
+}
+
+// Partners of row x along consecutive phases (in-sweep phase ph = 0..m, m = the
+// diagonal, where the "partner" is x itself), division-free after the first:
+// circle_partner(x, k) - 1 = (3m - x - 1 - 2k) mod m steps by -2 per colour (-1 for
+// id 0), and the diagonal phase does not advance k (k = m is k = 0 mod m).
+struct PartnerWalk {
+    int x, m, v, ph;
+    __device__ __forceinline__ PartnerWalk(int x_, int ph_, int m_) : x(x_), m(m_), ph(ph_) {
+        const int k = (ph_ == m_) ? 0 : ph_;
+        v = (x_ == 0) ? (m_ - 1 - k) % m_ : (3 * m_ - x_ - 1 - 2 * k) % m_;
+    }
+    __device__ __forceinline__ int y() const {
+        if (ph == m) return x;
+        return (x != 0 && 1 + v == x) ? 0 : 1 + v;
+    }
+    __device__ __forceinline__ void next() {
+        if (ph == m) {
+            ph = 0;
+        } else {
+            ++ph;
+            v -= (x == 0) ? 1 : 2;
+            if (v < 0) v += m;
+        }
+    }
+};
+
+// ld.global.cg of a double when `on`, else 0.0, without a branch.
+__device__ __forceinline__ double ldcg_if(const double* ptr, bool on) {
+    double v;
+    asm volatile(
+        "{\n .reg .pred pp;\n setp.ne.b32 pp, %2, 0;\n mov.f64 %0, 0d0000000000000000;\n"
+        " @pp ld.global.cg.f64 %0, [%1];\n}"
+        : "=d"(v)
+        : "l"(ptr), "r"((int)on));
     return v;
 }
 
@@ -84,8 +134,10 @@ __device__ __forceinline__ Blk block_at(int b, int m, int D, int NB) {
     return k;
 }
 // Watermark of the stage of block b: every phase <= C' is already in the staged cells.
+// C'(b) = start of block b-3, minus one: the deltas it needs are known once the chain is at
+// block b-3, so the stager has a block of slack before the chain needs it (at block b-2).
 __device__ __forceinline__ int stage_mark(int b, int m, int D, int NB) {
-    return (b < 2) ? -1 : block_at(b - 2, m, D, NB).g0 - 1;
+    return (b < 3) ? -1 : block_at(b - 3, m, D, NB).g0 - 1;
 }
 
 // Exclusive scan of s[0..n) in place by the apply warps; returns the total (also in s[n]).
@@ -164,6 +216,151 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
     }
 }
 
+// Same row streams, with the loads moved off the register file: every apply
+// thread keeps kAsyncStages items in flight through its own ring of
+// shared-memory slots (cp.async, 32 B per item: the W and T chunk), so an SM
+// holds kApply * kAsyncStages * 32 B of row traffic in flight instead of the
+// 2 * kRowUnroll double2 pairs the registers allow. Each thread only reads the
+// slots it filled, so no barrier is needed; cp.async.wait_group orders them.
+// The item -> (entry, half, chunk) mapping and the FMA are those of apply_rows.
+#if QB_ASYNC_STAGES > 0
+__device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double* L_d, const int* L_ph, int only,
+                                                 int e_lo, int e_hi, int w2, double* __restrict__ Wb,
+                                                 const double* __restrict__ Tb, double2* ring, int ta) {
+    const int per = 2 * w2;
+    const int items = (e_hi - e_lo) * per;
+    const int nmine = items > ta ? (items - ta + kApply - 1) / kApply : 0;
+    auto locate = [&](int i, int& e, int& off_w, int& off_t) {
+        const int idx = ta + i * kApply;
+        const int q = idx / per;
+        e = e_lo + q;
+        const int rem = idx - q * per;
+        const int h = rem >= w2;
+        const int j2 = rem - h * w2;
+        const int2 rs = L_rs[e];
+        off_w = (h ? rs.y : rs.x) * w2 + j2;
+        off_t = (h ? rs.x : rs.y) * w2 + j2;
+    };
+    auto issue = [&](int i) {
+        int e, ow, ot;
+        locate(i, e, ow, ot);
+        if (only < 0 || L_ph[e] == only) {
+            double2* slot = ring + (size_t)((i % kAsyncStages) * 2) * kApply + ta;
+            const unsigned sw = (unsigned)__cvta_generic_to_shared(slot);
+            const unsigned st = (unsigned)__cvta_generic_to_shared(slot + kApply);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sw),
+                         "l"(reinterpret_cast<const double2*>(Wb) + ow)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st),
+                         "l"(reinterpret_cast<const double2*>(Tb) + ot)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // prologue: kAsyncStages - 1 items in flight; then one issue per completed item,
+    // and in the tail (nothing left to issue) wait for everything.
+    int ni = min(nmine, kAsyncStages - 1);
+    for (int i = 0; i < ni; ++i) issue(i);
+    for (int j = 0; j < nmine; ++j) {
+        if (ni < nmine) {
+            issue(ni++);
+            asm volatile("cp.async.wait_group %0;" ::"n"(kAsyncStages - 1) : "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        int e, ow, ot;
+        locate(j, e, ow, ot);
+        if (only < 0 || L_ph[e] == only) {
+            const double2* slot = ring + (size_t)((j % kAsyncStages) * 2) * kApply + ta;
+            double2 wv = slot[0];
+            const double2 tv = slot[kApply];
+            const double d = L_d[e];
+            wv.x = fma(d, tv.x, wv.x);
+            wv.y = fma(d, tv.y, wv.y);
+            reinterpret_cast<double2*>(Wb)[ow] = wv;
+        }
+    }
+}
+#endif
+
+
+// Rows of a batch whose phases move some row more than once (entries [0, nent), all in
+// shared memory, phase L_ph).  Every half-entry (dst row, src row, delta) is linked to the
+// next half-entry of the batch with the same dst row (phase order); the first of each chain
+// loads W[dst, chunk] once, the T chunks of the whole chain at once, and applies the FMAs in
+// phase order -- the same operations, in the same order, as phase-by-phase passes, in one
+// round trip instead of one per phase.
+__device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d, const int* L_ph, int nent, int w2,
+                                             double* __restrict__ Wb, const double* __restrict__ Tb, short* s_next,
+                                             unsigned char* s_first, int ta) {
+    for (int he = ta; he < 2 * nent; he += kApply) {
+        const int e = he >> 1;
+        const int2 rs = L_rs[e];
+        const int dst = (he & 1) ? rs.y : rs.x;
+        const int ph = L_ph[e];
+        int nxt = -1, nph = 0x7fffffff;
+        bool first = true;
+        for (int e2 = 0; e2 < nent; ++e2) {
+            const int2 r2 = L_rs[e2];
+            const int ph2 = L_ph[e2];
+            if (r2.x == dst || r2.y == dst) {
+                if (ph2 < ph) first = false;
+                else if (ph2 > ph && ph2 < nph) {
+                    nph = ph2;
+                    nxt = 2 * e2 + (r2.y == dst ? 1 : 0);
+                }
+            }
+        }
+        s_next[he] = (short)nxt;
+        s_first[he] = first ? 1 : 0;
+    }
+    bar_apply();
+    const int items = 2 * nent * w2;
+    for (int idx = ta; idx < items; idx += kApply) {
+        const int he = idx / w2;
+        if (!s_first[he]) continue;
+        const int j2 = idx - he * w2;
+        const int2 rs0 = L_rs[he >> 1];
+        const int dst = (he & 1) ? rs0.y : rs0.x;
+        double2* wp = reinterpret_cast<double2*>(Wb) + (long long)dst * w2 + j2;
+        double2 wv = __ldcg(wp);
+        // the chain, four links at a time: T loads of a group back to back, then its FMAs
+        int k = he;
+        while (k >= 0) {
+            int srcs[4];
+            double ds[4];
+            int len = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k >= 0) {
+                    const int2 r = L_rs[k >> 1];
+                    srcs[u] = (k & 1) ? r.x : r.y;
+                    ds[u] = L_d[k >> 1];
+                    len = u + 1;
+                    k = s_next[k];
+                }
+            }
+            double2 tv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < len) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb) + (long long)srcs[u] * w2 + j2);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < len) {
+                    wv.x = fma(ds[u], tv[u].x, wv.x);
+                    wv.y = fma(ds[u], tv[u].y, wv.y);
+                }
+        }
+        *wp = wv;
+    }
+}
+
+#if QB_ASYNC_STAGES > 0
+#define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) \
+    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_)
+#else
+#define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) apply_rows(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ta_)
+#endif
 
 __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target) {
     unsigned long long v;
@@ -172,6 +369,11 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsi
     } while (v < target);
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+
+struct Layout {
+    int lo[kDMax], cb[kDMax + 1], slot[kDMax + 1], rdc[kDMax], lsl[kDMax];
+    int ncell, rd0, ph0w, rdb, phb;
+};
 
 struct Smem {
     int2* L_rs;     // [kPairCap]  delta-list chunk
@@ -182,20 +384,27 @@ struct Smem {
     unsigned* bm;   // [(p + 31) / 32]
     double* td;     // [p] T diagonal, or NULL
     int* cX;        // [cellcap] row of each block cell (-1: phantom)
+    int* cC;        // [cellcap] column of each block cell
     double* cW;     // [cellcap] cell value brought forward to the start of the block
     double* cO;     // [cellcap] Omega of the cell
     double* cT;     // [cellcap][kDMax-1] T entries of the block's earlier phases
     double* sd;     // [kDMax][rmax] delta of each pair of the block's phases (extended ranges)
     short* cQ;      // [cellcap][kDMax-1] index into sd[i] of the cell row's pair at in-block phase i
+    double* snv;    // [kDMax][share] new value of each own pair of the block's colours
+    int2* hd_rs;    // [kBatch * nblk] first entry of each list segment of a batch
+    double2* hd_dn; // [kBatch * nblk]
+    double2* ring;  // [kAsyncStages][2][kApply] per-thread cp.async slots of the row streams
 };
 
 __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_epoch, s_blk, s_stop, s_staged, s_iters, s_conv;
-    __shared__ int s_cnt[2];
+    __shared__ int s_cnt[kDMax];
+    __shared__ short s_next[2 * kChainN];
+    __shared__ unsigned char s_first[2 * kChainN];
     __shared__ int s_aE, s_aBlk, s_aStop, s_nent, s_multi, s_conflict;
     __shared__ int s_wsum[kApplyWarps];
-    __shared__ int s_lo[kDMax], s_cb[kDMax + 1], s_slot[kDMax + 1], s_ncell, s_rd0, s_ph0w;
+    __shared__ Layout s_ly[2];
     __shared__ double s_red[4][kApplyWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -226,12 +435,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         sm.L_ph = reinterpret_cast<int*>(take(sizeof(int) * kPairCap));
         sm.s_off = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)kBatch * nblk + 1)));
         sm.bm = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (size_t)((p + 31) / 32)));
-        sm.cX = reinterpret_cast<int*>(take(sizeof(int) * (size_t)a.cellcap));
-        sm.cW = reinterpret_cast<double*>(take(sizeof(double) * (size_t)a.cellcap));
-        sm.cO = reinterpret_cast<double*>(take(sizeof(double) * (size_t)a.cellcap));
-        sm.cT = reinterpret_cast<double*>(take(sizeof(double) * (size_t)a.cellcap * (kDMax - 1)));
+        sm.cX = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)a.cellcap));
+        sm.cC = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)a.cellcap));
+        sm.cW = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)a.cellcap));
+        sm.cO = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)a.cellcap));
+        sm.cT = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)a.cellcap * (kDMax - 1)));
         sm.sd = reinterpret_cast<double*>(take(sizeof(double) * (size_t)kDMax * a.rmax));
-        sm.cQ = reinterpret_cast<short*>(take(sizeof(short) * (size_t)a.cellcap * (kDMax - 1)));
+        sm.cQ = reinterpret_cast<short*>(take(sizeof(short) * 2 * (size_t)a.cellcap * (kDMax - 1)));
+        sm.snv = reinterpret_cast<double*>(take(sizeof(double) * (size_t)kDMax * a.share));
+        sm.hd_rs = reinterpret_cast<int2*>(take(sizeof(int2) * (size_t)kBatch * nblk));
+        sm.hd_dn = reinterpret_cast<double2*>(take(sizeof(double2) * (size_t)kBatch * nblk));
+        sm.ring = kAsyncStages ? reinterpret_cast<double2*>(take(sizeof(double2) * 2 * (size_t)kApply * kAsyncStages)) : nullptr;
         sm.td = a.tdiag_smem ? reinterpret_cast<double*>(take(sizeof(double) * (size_t)p)) : nullptr;
     }
     if (sm.td)
@@ -262,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         s_blk = -1;
         s_stop = -1;
         s_staged = 1;
-        s_cnt[0] = s_cnt[1] = 0;
+        for (int d = 0; d < kDMax; ++d) s_cnt[d] = 0;
         s_conflict = 0;
     }
     __syncthreads();
@@ -272,12 +486,149 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     if (warp < kChainWarps) {
         // ================================================================ chain warps
         const int tc = tid;
+        // The colours of a block need one thread per pair of the widest colour (own pairs plus
+        // halo): the last ncw chain warps (the colour group).  The other chain warps (the
+        // prefetch group) meanwhile build part A of the next block's cells, so only part B
+        // (the previous block's deltas) is left between a barrier and the colours.  When the
+        // colours need every chain warp, part A runs after the arrive instead.
+        const int ncw = min(kChainWarps, (a.share + 2 * (D - 1) + 31) / 32);
+        const bool overlap = ncw < kChainWarps;
+        const int cg0 = kChain - 32 * ncw;  // first thread of the colour group
+        const int ng = 32 * ncw;
+        const bool in_cg = tc >= cg0;
+        const int gt = tc - cg0;  // thread index in the colour group
+        auto bar_colour = [&]() {
+            if (overlap) asm volatile("bar.sync 3, %0;" ::"r"(ng) : "memory");
+            else bar_chain();
+        };
         bar_chain();
         if (tc == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
         if (b == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
         double smax = 0.0;  // max |delta| of this thread's own pairs over the sweep
         int snnz = 0;
-        long long t_wait = 0, t_load = 0, t_work = 0, t_c0 = 0, t_c1 = 0, t_c2 = 0, t_c3 = 0;
+        long long t_wait = 0, t_load = 0, t_work = 0, t_c0 = 0, t_c3 = 0;
+        long long t_q0 = 0, t_q1 = 0, t_q2 = 0;  // colour sub-steps of the thread of the first pair
+        // Cells of block B, part A -- everything that does not depend on the deltas of block
+        // B-1: layout, stage values (watermark C'(B) = start of block B-3, minus one), in-block
+        // T entries and pair slots, and the deltas of blocks B-3, B-2 (phases C'(B)+1 .. g0(B-1)-1).
+        // Part B (after the barrier of block B) folds in the deltas of block B-1, in phase
+        // order.  Blocks alternate between two cell buffers and two layouts.  Threads
+        // [0, gs) take part, synchronised by the named barrier `bar_id`.
+        auto cells_a = [&](int B, int gs, int bar_id) {
+            const Blk kB = block_at(B, m, D, NB);
+            const bool hdB = (kB.ph0 + kB.len - 1 == m);
+            const int nbcB = kB.len - (hdB ? 1 : 0);
+            const int CpB = stage_mark(B, m, D, NB);
+            const int hiA = (B >= 1) ? block_at(B - 1, m, D, NB).g0 : 0;
+            const int na = hiA - (CpB + 1);
+            Layout& L = s_ly[B & 1];
+            const int cb = (B & 1) * a.cellcap;
+            // layout: colour d = 0..nbc-1 covers pairs [lo_d, hi_d), two cells per pair;
+            // then the diagonal cells (rows of the own pairs at colour m-1)
+            if (tc == 0) {
+                int nc = 0;
+                for (int d = 0; d < kDMax; ++d) {
+                    const int h = nbcB - 1 - d;
+                    L.lo[d] = (d < nbcB) ? max(0, q_lo - h) : 0;
+                    const int hi = (d < nbcB) ? min(half, q_hi + h) : 0;
+                    L.cb[d] = nc;
+                    nc += (d < nbcB) ? 2 * (hi - L.lo[d]) : 0;
+                }
+                L.cb[kDMax] = nc;
+                L.ncell = nc;
+                for (int d = 0; d <= kDMax; ++d) L.slot[d] = (kB.g0 + d) % a.sr;
+                for (int d = 0; d < kDMax; ++d) {
+                    L.rdc[d] = (kB.g0 + d) % a.rd;
+                    L.lsl[d] = (kB.g0 + d) % a.rl;
+                }
+                L.rd0 = (CpB + 1) % a.rd;
+                L.ph0w = (CpB + 1) % (m + 1);
+                L.rdb = hiA % a.rd;
+                L.phb = hiA % (m + 1);
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gs) : "memory");
+            const int ncellB = L.ncell;
+            const int ntotB = ncellB + (hdB ? 2 * (q_hi - q_lo) : 0);
+            for (int ci = tc; ci < ntotB; ci += gs) {
+                int d, x, c;
+                if (ci < ncellB) {
+                    d = 0;
+                    while (d + 1 < nbcB && ci >= L.cb[d + 1]) ++d;
+                    const int rel = ci - L.cb[d];
+                    const int q = L.lo[d] + (rel >> 1);
+                    int r, s2;
+                    round_pair(q, m, m - 1 - (kB.ph0 + d), r, s2);
+                    if (s2 >= p) {
+                        sm.cX[cb + ci] = -1;
+                        continue;
+                    }
+                    x = (rel & 1) ? s2 : r;
+                    c = (rel & 1) ? r : s2;
+                } else {
+                    d = nbcB;
+                    const int rel = ci - ncellB;
+                    const int q = q_lo + (rel >> 1);
+                    int r, s2;
+                    round_pair(q, m, 0, r, s2);  // colour m-1
+                    x = (rel & 1) ? s2 : r;
+                    if (x >= p) {
+                        sm.cX[cb + ci] = -1;
+                        continue;
+                    }
+                    c = x;
+                }
+                const int cs = c / w;  // slab of column c
+                const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
+                const size_t so = (size_t)L.slot[d] * p + c;
+                double val = __ldcg(a.stW + so);
+                const double om = __ldcg(a.stO + so);
+                // in-block phases ph0 .. ph0+d-1: T entries staged by the slab owner; the row's
+                // pair index (into sd) stepped without division
+                double tin[kDMax - 1];
+#pragma unroll
+                for (int i = 0; i < kDMax - 1; ++i)
+                    tin[i] = ldcg_if(a.stT + ((size_t)L.slot[d] * (kDMax - 1) + i) * p + c, i < d);
+                {
+                    int pos = (x == 0) ? 0 : 1 + (x - 1 + kB.ph0) % m;
+                    for (int i = 0; i < d; ++i) {
+                        const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
+                        sm.cQ[(size_t)(cb + ci) * (kDMax - 1) + i] = (short)(qi - L.lo[i]);
+                        if (x != 0) pos = (pos == m) ? 1 : pos + 1;
+                    }
+                }
+                // deltas of blocks B-3 and B-2: ring loads back to back; T entries (HBM) only for
+                // the phases that moved row x, again back to back; then the FMAs in phase order
+                double dj[2 * kDMax];
+                int slot = L.rd0;
+#pragma unroll
+                for (int u = 0; u < 2 * kDMax; ++u) {
+                    dj[u] = ldcg_if(a.dring + (size_t)slot * p + x, u < na);
+                    slot = (slot + 1 == a.rd) ? 0 : slot + 1;
+                }
+                unsigned mask = 0u;
+#pragma unroll
+                for (int u = 0; u < 2 * kDMax; ++u)
+                    if (dj[u] != 0.0) mask |= 1u << u;
+                if (mask) {
+                    double tj[2 * kDMax];
+                    PartnerWalk pw(x, L.ph0w, m);
+#pragma unroll
+                    for (int u = 0; u < 2 * kDMax; ++u) {
+                        tj[u] = ldcg_if(Tc + (long long)pw.y() * w, (mask >> u) & 1u);
+                        pw.next();
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2 * kDMax; ++u)
+                        if (mask & (1u << u)) val = fma(dj[u], tj[u], val);
+                }
+                sm.cX[cb + ci] = x;
+                sm.cC[cb + ci] = c;
+                sm.cW[cb + ci] = val;
+                sm.cO[cb + ci] = om;
+#pragma unroll
+                for (int i = 0; i < kDMax - 1; ++i) sm.cT[(size_t)(cb + ci) * (kDMax - 1) + i] = tin[i];
+            }
+        };
         int blk = 0;
         while (true) {
             const long long t0 = clock64();
@@ -313,263 +664,248 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             }
             const bool has_diag = (k.ph0 + k.len - 1 == m);
             const int nbc = k.len - (has_diag ? 1 : 0);  // colour phases of the block
-            const int Cp = stage_mark(blk, m, D, NB);
-            // cell layout: colour d = 0..nbc-1 covers pairs [lo_d, hi_d), two cells per pair;
-            // then the diagonal cells (rows of the own pairs at colour m-1)
-            if (tc == 0) {
-                int nc = 0;
-                for (int d = 0; d < kDMax; ++d) {
-                    const int h = nbc - 1 - d;
-                    s_lo[d] = (d < nbc) ? max(0, q_lo - h) : 0;
-                    const int hi = (d < nbc) ? min(half, q_hi + h) : 0;
-                    s_cb[d] = nc;
-                    nc += (d < nbc) ? 2 * (hi - s_lo[d]) : 0;
-                }
-                s_cb[kDMax] = nc;
-                s_ncell = nc;
-                for (int d = 0; d <= kDMax; ++d) s_slot[d] = (k.g0 + d) % a.sr;
-                s_rd0 = (Cp + 1) % a.rd;
-                s_ph0w = (Cp + 1) % (m + 1);
+            const Layout& L = s_ly[blk & 1];
+            const int cb = (blk & 1) * a.cellcap;
+            if (blk == 0) {
+                cells_a(0, kChain, 1);
+                bar_chain();
             }
-            bar_chain();
-            const int ncell = s_ncell;
-            const int ndiag = has_diag ? 2 * (q_hi - q_lo) : 0;
-            const int ntot = ncell + ndiag;
-
-            // ---- cells: stage value, deltas of the two previous blocks, T entries of this block
-            for (int ci = tc; ci < ntot; ci += kChain) {
-                int d, x, c;
-                if (ci < ncell) {
-                    d = 0;
-                    while (d + 1 < nbc && ci >= s_cb[d + 1]) ++d;
-                    const int rel = ci - s_cb[d];
-                    const int q = s_lo[d] + (rel >> 1);
-                    int r, s2;
-                    round_pair(q, m, m - 1 - (k.ph0 + d), r, s2);
-                    if (s2 >= p) {
-                        sm.cX[ci] = -1;
-                        continue;
-                    }
-                    x = (rel & 1) ? s2 : r;
-                    c = (rel & 1) ? r : s2;
-                } else {
-                    d = nbc;
-                    const int rel = ci - ncell;
-                    const int q = q_lo + (rel >> 1);
-                    int r, s2;
-                    round_pair(q, m, 0, r, s2);  // colour m-1
-                    x = (rel & 1) ? s2 : r;
-                    if (x >= p) {
-                        sm.cX[ci] = -1;
-                        continue;
-                    }
-                    c = x;
-                }
-                const long long tq0 = clock64();
-                const int cs = c / w;  // slab of column c
-                const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
-                const size_t so = (size_t)s_slot[d] * p + c;
-                double val = __ldcg(a.stW + so);
-                const double om = __ldcg(a.stO + so);
-                // in-block phases ph0 .. ph0+d-1 (all colours): the row's partner (T entry, loaded
-                // unconditionally) and the row's pair index (into sd), both stepped without division
-                // in-block phases ph0 .. ph0+d-1 (all colours): T entries staged by the slab owner;
-                // the row's pair index (into sd) stepped without division
-                double tin[kDMax - 1];
+            // ---- cells, part B (on the critical path): deltas of the previous block
+            {
+                const int hiA = (blk >= 1) ? block_at(blk - 1, m, D, NB).g0 : 0;
+                const int nbv = k.g0 - hiA;
+                const int ntotB = L.ncell + (has_diag ? 2 * (q_hi - q_lo) : 0);
+                for (int ci = tc; ci < ntotB; ci += kChain) {
+                    const int x = sm.cX[cb + ci];
+                    if (x < 0) continue;
+                    double dj[kDMax];
+                    int slot = L.rdb;
 #pragma unroll
-                for (int i = 0; i < kDMax - 1; ++i)
-                    tin[i] = (i < d) ? __ldcg(a.stT + ((size_t)s_slot[d] * (kDMax - 1) + i) * p + c) : 0.0;
-                {
-                    int pos = (x == 0) ? 0 : 1 + (x - 1 + k.ph0) % m;
-                    for (int i = 0; i < d; ++i) {
-                        const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
-                        sm.cQ[(size_t)ci * (kDMax - 1) + i] = (short)(qi - s_lo[i]);
-                        if (x != 0) pos = (pos == m) ? 1 : pos + 1;
-                    }
-                }
-                const long long tq1 = clock64();
-                // deltas of the phases Cp+1 .. g0-1 (the two previous blocks): which moved row x?
-                // The (rare) corrections themselves need T entries from HBM: they are applied in a
-                // second pass over the flagged cells, all in parallel.
-                // all delta loads first (predicated, back to back); then, for the phases that moved
-                // row x, the T entries (HBM), again back to back; then the FMAs in phase order
-                {
-                    double dj[2 * kDMax];
-                    int slot = s_rd0;
-#pragma unroll
-                    for (int u = 0; u < 2 * kDMax; ++u) {
-                        const bool in = Cp + 1 + u < k.g0;
-                        dj[u] = in ? __ldcg(a.dring + (size_t)slot * p + x) : 0.0;
+                    for (int u = 0; u < kDMax; ++u) {
+                        dj[u] = ldcg_if(a.dring + (size_t)slot * p + x, u < nbv);
                         slot = (slot + 1 == a.rd) ? 0 : slot + 1;
                     }
                     unsigned mask = 0u;
 #pragma unroll
-                    for (int u = 0; u < 2 * kDMax; ++u)
+                    for (int u = 0; u < kDMax; ++u)
                         if (dj[u] != 0.0) mask |= 1u << u;
                     if (mask) {
-                        double tj[2 * kDMax];
-                        int phw = s_ph0w;
+                        const int c = sm.cC[cb + ci];
+                        const int cs = c / w;  // slab of column c
+                        const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
+                        double tj[kDMax];
+                        PartnerWalk pw(x, L.phb, m);
 #pragma unroll
-                        for (int u = 0; u < 2 * kDMax; ++u) {
-                            const bool on = (mask & (1u << u)) != 0;
-                            const int y = on ? src_row(phw, x, m) : x;
-                            tj[u] = on ? __ldcg(Tc + (long long)y * w) : 0.0;
-                            phw = (phw == m) ? 0 : phw + 1;
+                        for (int u = 0; u < kDMax; ++u) {
+                            tj[u] = ldcg_if(Tc + (long long)pw.y() * w, (mask >> u) & 1u);
+                            pw.next();
                         }
+                        double val = sm.cW[cb + ci];
 #pragma unroll
-                        for (int u = 0; u < 2 * kDMax; ++u)
+                        for (int u = 0; u < kDMax; ++u)
                             if (mask & (1u << u)) val = fma(dj[u], tj[u], val);
+                        sm.cW[cb + ci] = val;
                     }
-                }
-                const long long tq2 = clock64();
-                sm.cX[ci] = x;
-                sm.cW[ci] = val;
-                sm.cO[ci] = om;
-#pragma unroll
-                for (int i = 0; i < kDMax - 1; ++i) sm.cT[(size_t)ci * (kDMax - 1) + i] = tin[i];
-                if (tc == 0) {
-                    const long long tq3 = clock64();
-                    t_c0 += tq1 - tq0;
-                    t_c1 += tq2 - tq1;
-                    t_c2 += tq3 - tq2;
                 }
             }
             bar_chain();
-            bar_chain();
+            const int ncell = L.ncell;
+            const int ndiag = has_diag ? 2 * (q_hi - q_lo) : 0;
             const long long t2 = clock64();
             t_load += t2 - t1;
 
-            // ---- the block's colours, in order, in shared memory
-            for (int d = 0; d < nbc; ++d) {
-                const int ph = k.ph0 + d;
-                const int Q = k.g0 + d;
-                const int h = nbc - 1 - d;
-                const int hi = min(half, q_hi + h);
-                const int lod = s_lo[d], cbd = s_cb[d];
-                const int c1 = m - 1 - ph;
-                const int lslot = Q % a.rl;
-                const size_t dgo = (size_t)(Q % a.rd) * p;  // once per colour
-                const size_t seg_off = ((size_t)lslot * nblk + b) * a.share;
-                double* sdd = sm.sd + (size_t)d * a.rmax;
-                const int sid = kChain - 1 - tc;
-                for (int base = lod; base < hi; base += kChain) {
-                    const int q = base + sid;
-                    int r = 0, s = 0;
-                    double dl = 0.0, nv = 0.0;
-                    const bool own = q >= q_lo && q < q_hi;
-                    if (q < hi) {
+            if (in_cg) {
+                // ---- the block's colours, in order, in shared memory; only the deltas (sd) and
+                // the new values of the own pairs (snv) are written per colour, the ring and the
+                // lists after the last colour
+                for (int d = 0; d < nbc; ++d) {
+                    const int ph = k.ph0 + d;
+                    const int h = nbc - 1 - d;
+                    const int hi = min(half, q_hi + h);
+                    const int lod = L.lo[d], cbd = cb + L.cb[d];
+                    const int c1 = m - 1 - ph;
+                    double* sdd = sm.sd + (size_t)d * a.rmax;
+                    const int sid = ng - 1 - gt;
+                    for (int base = lod; base < hi; base += ng) {
+                        const int q = base + sid;
+                        if (q >= hi) continue;
+                        long long tp0 = 0, tp1 = 0, tp2 = 0;
+                        if (prof && sid == 0) tp0 = clock64();
+                        int r, s;
                         round_pair(q, m, c1, r, s);
+                        double dl = 0.0, nv = 0.0;
                         if (s < p) {
                             const int ci = cbd + 2 * (q - lod);
-                            double v2[2];
+                            // corrections of the block's earlier colours, three rounds of shared
+                            // loads (pair slots, deltas, T entries) for both cells, then the FMAs
+                            // in colour order
+                            short qi[2][kDMax - 1];
+                            double di[2][kDMax - 1], ti[2][kDMax - 1], v2[2];
 #pragma unroll
                             for (int side = 0; side < 2; ++side) {
-                                const int cc = ci + side;
-                                const int x = sm.cX[cc];
-                                double val = sm.cW[cc];
-                                (void)x;
-                                for (int i = 0; i < d; ++i) {
-                                    const double di = sm.sd[(size_t)i * a.rmax + sm.cQ[(size_t)cc * (kDMax - 1) + i]];
-                                    if (di != 0.0) val = fma(di, sm.cT[(size_t)cc * (kDMax - 1) + i], val);
-                                }
-                                v2[side] = val;
+                                v2[side] = sm.cW[ci + side];
+#pragma unroll
+                                for (int i = 0; i < kDMax - 1; ++i)
+                                    qi[side][i] = (i < d) ? sm.cQ[(size_t)(ci + side) * (kDMax - 1) + i] : (short)0;
                             }
+#pragma unroll
+                            for (int side = 0; side < 2; ++side)
+#pragma unroll
+                                for (int i = 0; i < kDMax - 1; ++i) {
+                                    di[side][i] = (i < d) ? sm.sd[(size_t)i * a.rmax + qi[side][i]] : 0.0;
+                                    ti[side][i] = (i < d) ? sm.cT[(size_t)(ci + side) * (kDMax - 1) + i] : 0.0;
+                                }
+#pragma unroll
+                            for (int side = 0; side < 2; ++side)
+#pragma unroll
+                                for (int i = 0; i < kDMax - 1; ++i)
+                                    if (i < d && di[side][i] != 0.0) v2[side] = fma(di[side][i], ti[side][i], v2[side]);
                             // side 0: cell (r, s) = W[r,s]; side 1: cell (s, r) = W[s,r]
                             const double om = sm.cO[ci];
-                            dl = pair_delta(make_double2(v2[1], om), make_double2(v2[0], om), TD(r), TD(s), a.shrink, nv);
-                            if (own) {
-                                a.dring[dgo + r] = dl;
-                                a.dring[dgo + s] = dl;
-                                if (dl != 0.0) {
-                                    smax = fmax(smax, fabs(dl));
-                                    ++snnz;
-                                }
-                            }
-                        } else if (own) {
-                            a.dring[dgo + r] = 0.0;  // partner is the phantom (odd p)
+                            if (prof && sid == 0) tp1 = clock_after(v2[0] + v2[1]);
+                            dl = pair_delta(make_double2(v2[1], om), make_double2(v2[0], om), TD(r), TD(s), a.shrink,
+                                            nv);
+                            if (prof && sid == 0) tp2 = clock_after(dl);
                         }
                         sdd[q - lod] = dl;
+                        if (q >= q_lo && q < q_hi) sm.snv[d * a.share + (q - q_lo)] = nv;
+                        if (prof && sid == 0 && tp2 != 0) {
+                            const long long tp3 = clock64();
+                            t_q0 += tp1 - tp0;
+                            t_q1 += tp2 - tp1;
+                            t_q2 += tp3 - tp2;
+                        }
                     }
-                    const bool nz = own && dl != 0.0;
-                    const unsigned mask = __ballot_sync(0xffffffffu, nz);
-                    if (mask) {
-                        int basepos = 0;
-                        if (lane == 0) basepos = atomicAdd(&s_cnt[d & 1], __popc(mask));
-                        basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                    bar_colour();
+                }
+                // ---- publish the own pairs of all colours: delta ring, non-zero delta lists
+                {
+                    const int nown = q_hi - q_lo;
+                    for (int base = 0; base < nbc * nown; base += ng) {
+                        const int idx = base + gt;
+                        const bool live = idx < nbc * nown;
+                        int d = 0, q = 0, r = 0, s = 0;
+                        double dl = 0.0, nv = 0.0;
+                        if (live) {
+                            d = idx / nown;
+                            q = q_lo + (idx - d * nown);
+                            round_pair(q, m, m - 1 - (k.ph0 + d), r, s);
+                            dl = sm.sd[(size_t)d * a.rmax + (q - L.lo[d])];
+                            nv = sm.snv[d * a.share + (q - q_lo)];
+                            const size_t dgo = (size_t)L.rdc[d] * p;
+                            a.dring[dgo + r] = dl;  // 0 when the partner is the phantom (odd p)
+                            if (s < p) a.dring[dgo + s] = dl;
+                            if (dl != 0.0) {
+                                smax = fmax(smax, fabs(dl));
+                                ++snnz;
+                            }
+                        }
+                        const bool nz = live && dl != 0.0;
+                        // one warp-aggregated slot reservation per colour present in the warp
+                        unsigned pending = __ballot_sync(0xffffffffu, nz);
+                        int at = 0;
+                        while (pending) {
+                            const int leader = __ffs(pending) - 1;
+                            const int dd = __shfl_sync(0xffffffffu, d, leader);
+                            const unsigned mm = __ballot_sync(0xffffffffu, nz && d == dd);
+                            int basepos = 0;
+                            if (lane == leader) basepos = atomicAdd(&s_cnt[dd], __popc(mm));
+                            basepos = __shfl_sync(0xffffffffu, basepos, leader);
+                            if (nz && d == dd) at = basepos + __popc(mm & ((1u << lane) - 1u));
+                            pending &= ~mm;
+                        }
                         if (nz) {
-                            const int at = basepos + __popc(mask & ((1u << lane) - 1u));
+                            const size_t seg_off = ((size_t)L.lsl[d] * nblk + b) * a.share;
                             a.list_rs[seg_off + at] = make_int2(r, s);
                             a.list_dn[seg_off + at] = make_double2(dl, nv);
                         }
                     }
+                    bar_colour();
+                    if (gt == 0) {  // the thread that arrives: its own stores are ordered by the release
+                        for (int d = 0; d < nbc; ++d) {
+                            a.list_cnt[(size_t)L.lsl[d] * nblk + b] = s_cnt[d];
+                            s_cnt[d] = 0;
+                        }
+                    }
                 }
-                bar_chain();
-                if (tc == 0) {
-                    a.list_cnt[(size_t)lslot * nblk + b] = s_cnt[d & 1];
-                    s_cnt[d & 1] = 0;
-                }
-            }
 
-            // ---- diagonal phase (closes the sweep): rows of the own pairs at colour m-1
-            if (has_diag) {
-                const int Qd = k.g0 + nbc;
-                const size_t dgo = (size_t)(Qd % a.rd) * p;
-                double dm = 0.0;
-                for (int e = tc; e < ndiag; e += kChain) {
-                    const int cc = ncell + e;
-                    const int x = sm.cX[cc];
-                    if (x < 0) continue;
-                    double val = sm.cW[cc];
-                    for (int i = 0; i < nbc; ++i) {
-                        const double di = sm.sd[(size_t)i * a.rmax + sm.cQ[(size_t)cc * (kDMax - 1) + i]];
-                        if (di != 0.0) val = fma(di, sm.cT[(size_t)cc * (kDMax - 1) + i], val);
+                // ---- diagonal phase (closes the sweep): rows of the own pairs at colour m-1
+                if (has_diag) {
+                    const int Qd = k.g0 + nbc;
+                    const size_t dgo = (size_t)(Qd % a.rd) * p;
+                    double dm = 0.0;
+                    for (int e = gt; e < ndiag; e += ng) {
+                        const int cc = cb + ncell + e;
+                        const int x = sm.cX[cc];
+                        if (x < 0) continue;
+                        double val = sm.cW[cc];
+                        for (int i = 0; i < nbc; ++i) {
+                            const double di = sm.sd[(size_t)i * a.rmax + sm.cQ[(size_t)cc * (kDMax - 1) + i]];
+                            if (di != 0.0) val = fma(di, sm.cT[(size_t)cc * (kDMax - 1) + i], val);
+                        }
+                        const double om = sm.cO[cc];
+                        const double nv = diag_from_dot(val, om, TD(x), a.n);
+                        const double dl = __dsub_rn(nv, om);
+                        a.dring[dgo + x] = dl;
+                        a.diagv[x] = make_double2(dl, nv);
+                        dm = fmax(dm, fabs(dl));
                     }
-                    const double om = sm.cO[cc];
-                    const double nv = diag_from_dot(val, om, TD(x), a.n);
-                    const double dl = __dsub_rn(nv, om);
-                    a.dring[dgo + x] = dl;
-                    a.diagv[x] = make_double2(dl, nv);
-                    dm = fmax(dm, fabs(dl));
-                }
-                // this sweep's statistics: off-diagonal (own pairs) and diagonal maxima, non-zero count
-                const double mw = warp_max(fmax(dm, smax));
-                const double nw = warp_sum((double)snnz);
-                if (lane == 0) {
-                    s_red[0][warp] = mw;
-                    s_red[1][warp] = nw;
-                }
-                smax = 0.0;
-                snnz = 0;
-                bar_chain();
-                if (tc == 0) {
-                    double mb = 0.0, nbk = 0.0;
-                    for (int j = 0; j < kChainWarps; ++j) {
-                        mb = fmax(mb, s_red[0][j]);
-                        nbk += s_red[1][j];
+                    // this sweep's statistics: off-diagonal (own pairs) and diagonal maxima, non-zero count
+                    const double mw = warp_max(fmax(dm, smax));
+                    const double nw = warp_sum((double)snnz);
+                    if (lane == 0) {
+                        s_red[0][warp] = mw;
+                        s_red[1][warp] = nw;
                     }
-                    atomicMax(a.dmax + (a.it_base + k.sweep) % WFORM_DMAX_RING, (unsigned long long)__double_as_longlong(mb));
-                    atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + k.sweep), (unsigned long long)nbk);
+                    smax = 0.0;
+                    snnz = 0;
+                    bar_colour();
+                    if (gt == 0) {
+                        double mb = 0.0, nbk = 0.0;
+                        for (int j = cg0 / 32; j < kChainWarps; ++j) {
+                            mb = fmax(mb, s_red[0][j]);
+                            nbk += s_red[1][j];
+                        }
+                        atomicMax(a.dmax + (a.it_base + k.sweep) % WFORM_DMAX_RING,
+                                  (unsigned long long)__double_as_longlong(mb));
+                        atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + k.sweep), (unsigned long long)nbk);
+                    }
+                }
+                if (gt == 0) t_work += clock64() - t2;
+                // ---- the block after next must be staged (by this CTA's apply warps) before
+                // arriving: part A of the next block's cells reads it before that block's barrier
+                if (gt == 0) {
+                    const long long tw0 = clock64();
+                    while (ld_acquire_cta(&s_staged) < blk + 2) {
+                    }
+                    t_c3 += clock64() - tw0;
+                    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
                 }
             }
-            t_work += clock64() - t2;
-            // ---- the next block's cells must be staged (by this CTA's apply warps) before arriving
-            if (tc == 0) {
-                const long long tw0 = clock64();
-                while (ld_acquire_cta(&s_staged) < blk + 1) {
-                }
-                t_c3 += clock64() - tw0;
-                asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
+            // ---- part A of the next block's cells: the prefetch group, concurrently with the
+            // colours (or every chain warp, after the arrive)
+            if (overlap ? !in_cg : true) {
+                const long long ta0 = clock64();
+                cells_a(blk + 1, overlap ? cg0 : kChain, overlap ? 4 : 1);
+                t_c0 += clock64() - ta0;
             }
+            bar_chain();
             ++blk;
         }
         if (prof && tc == 0) {
             prof[0] = (unsigned long long)t_wait;
             prof[1] = (unsigned long long)t_load;
-            prof[2] = (unsigned long long)t_work;
             prof[3] = (unsigned long long)blk;
             prof[7] = (unsigned long long)t_c0;
-            prof[8] = (unsigned long long)t_c1;
+        }
+        if (prof && tc == cg0) {
+            prof[2] = (unsigned long long)t_work;
             prof[9] = (unsigned long long)t_c3;
+        }
+        if (prof && tc == kChain - 1) {
+            prof[12] = (unsigned long long)t_q0;
+            prof[13] = (unsigned long long)t_q1;
+            prof[14] = (unsigned long long)t_q2;
         }
     } else {
         // ================================================================ apply warps
@@ -578,7 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         int cph = m;   // phase-in-sweep of C
         int cit = -1;  // sweep of C
         int staged = 1;  // highest block staged
-        long long t_busy = 0, t_idle = 0, nbatch = 0, t_diag = 0, t_stage = 0;
+        long long t_busy = 0, t_idle = 0, nbatch = 0, t_diag = 0, t_stage = 0, t_heads = 0, t_rows = 0;
         while (true) {
             const long long t0 = clock64();
             bar_apply();
@@ -592,6 +928,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 __threadfence_block();
             }
             bar_apply();
+            const long long th0 = clock64();
             const int E = s_aE;
             const int cblk = s_aBlk;
             const int stopg = s_aStop;
@@ -605,18 +942,40 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const int nb = k1 - C;
             const int nsh = nblk;
             const int nseg = nb * nsh;
-            // next block to stage: the chain at block cblk needs block cblk+1 before arriving;
-            // stage up to cblk+2.  Its watermark C' must be <= E-1 (deltas known) and the
+            // next block to stage: the chain at block cblk needs block cblk+2 before arriving;
+            // stage up to cblk+3.  Its watermark C' must be <= E-1 (deltas known) and the
             // window (C, C'] must still be in the delta ring.
             const int sb = staged + 1;
             const int Cp = stage_mark(sb, m, D, NB);
-            const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 2 && Cp <= E - 1 && C >= Cp - a.stage_window;
+            const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 3 && Cp <= E - 1 && C >= Cp - a.stage_window;
             if (!have && !can_stage) {
                 t_idle += clock64() - t0;
                 __nanosleep(32);
                 continue;
             }
 
+#if QB_ASYNC_HEADS
+            // ---- segment heads (count + first entry) of the batch's colours: copied
+            // asynchronously into shared memory while this thread stages (below); every
+            // thread then reads back only the heads it copied
+            for (int idx = ta; idx < nseg; idx += kApply) {
+                const int jb = idx / nsh;
+                const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                 (unsigned)__cvta_generic_to_shared(sm.s_off + idx)),
+                             "l"(lcntL + seg)
+                             : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                 (unsigned)__cvta_generic_to_shared(sm.hd_rs + idx)),
+                             "l"(lrsL + (size_t)seg * a.share)
+                             : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 (unsigned)__cvta_generic_to_shared(sm.hd_dn + idx)),
+                             "l"(ldnL + (size_t)seg * a.share)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+#else
             // ---- segment heads (count + first entry) of the batch's colours
             for (int idx = ta; idx < nseg; idx += kApply) {
                 const int jb = idx / nsh;
@@ -639,6 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
                 }
             }
+#endif
             // ---- stage block sb: cells brought forward from this slab's watermark C to C'
             if (can_stage) {
                 const long long ts = clock64();
@@ -651,17 +1011,33 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if (x < 0) continue;
                     double val = __ldcg(Wb + (long long)x * w + j);
                     const double om = __ldcg(Ob + (long long)x * w + j);
+                    // deltas of phases C+1 .. Cp, eight at a time: ring loads back to back, then the
+                    // T entries of the phases that moved row x (predicated, back to back), then the FMAs
+                    int rslot = (C + 1) % a.rd;
+                    PartnerWalk pw(x, (C + 1) % (m + 1), m);
                     for (int j0 = C + 1; j0 <= Cp; j0 += 8) {
-                        double dj[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            dj[u] = (j0 + u <= Cp) ? __ldcg(a.dring + (size_t)((j0 + u) % a.rd) * p + x) : 0.0;
+                        double dj[8], tj[8];
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            if (dj[u] != 0.0) {
-                                const int y = src_row((j0 + u) % (m + 1), x, m);
-                                val = fma(dj[u], __ldcg(Tb + (long long)y * w + j), val);
+                            dj[u] = ldcg_if(a.dring + (size_t)rslot * p + x, j0 + u <= Cp);
+                            rslot = (rslot + 1 == a.rd) ? 0 : rslot + 1;
+                        }
+                        unsigned mk = 0u;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (dj[u] != 0.0) mk |= 1u << u;
+                        if (mk) {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                tj[u] = ldcg_if(Tb + (long long)pw.y() * w + j, (mk >> u) & 1u);
+                                pw.next();
                             }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (mk & (1u << u)) val = fma(dj[u], tj[u], val);
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) pw.next();
                         }
                     }
                     const size_t so = (size_t)(Q % a.sr) * p + c;
@@ -683,7 +1059,30 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 }
                 t_stage += clock64() - ts;
             }
+#if QB_ASYNC_HEADS
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            for (int idx = ta; idx < nseg; idx += kApply) {
+                const int jb = idx / nsh;
+                const int cnt = sm.s_off[idx];
+                if (cnt > 1) s_multi = 1;
+                if (cnt == 1) {
+                    const int2 rs = sm.hd_rs[idx];
+                    const double2 dn = sm.hd_dn[idx];
+                    const int pos = atomicAdd(&s_nent, 1);
+                    if (pos < kPairCap) {
+                        sm.L_rs[pos] = rs;
+                        sm.L_d[pos] = dn.x;
+                        sm.L_ph[pos] = jb;
+                    } else {
+                        s_multi = 1;
+                    }
+                    if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
+                    if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                }
+            }
+#endif
             bar_apply();
+            const long long th1 = clock64();
             if (can_stage) {
                 staged = sb;
                 if (ta == 0) {
@@ -784,6 +1183,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 t_diag += clock64() - t0;
             } else if (nb > 0) {
                 // ---- colour phases k0 .. k1
+                t_heads += th1 - th0;
+                const long long tr0 = clock64();
                 int total = 0;
                 if (!s_multi) {
                     // every segment had at most one entry: they are already in shared memory
@@ -799,10 +1200,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         bar_apply();
                     }
                     if (!s_conflict) {
-                        apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, nent, w2, Wb, Tb, ta);
+                        ROWS(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, nent, w2, Wb, Tb, sm.ring, ta);
+                    } else if (nent <= kChainN) {
+                        apply_chains(sm.L_rs, sm.L_d, sm.L_ph, nent, w2, Wb, Tb, s_next, s_first, ta);
                     } else {
                         for (int jb = 0; jb < nb; ++jb) {  // rows repeat across phases: phase by phase
-                            apply_rows(sm.L_rs, sm.L_d, sm.L_ph, jb, 0, nent, w2, Wb, Tb, ta);
+                            ROWS(sm.L_rs, sm.L_d, sm.L_ph, jb, 0, nent, w2, Wb, Tb, sm.ring, ta);
                             bar_apply();
                         }
                     }
@@ -851,12 +1254,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         bar_apply();
                         const int conflict = s_conflict;
                         if (!conflict) {
-                            apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, e1 - e0, w2, Wb, Tb, ta);
+                            ROWS(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, e1 - e0, w2, Wb, Tb, sm.ring, ta);
                         } else {
                             for (int jb = 0; jb < nb; ++jb) {
                                 const int lo = max(sm.s_off[jb * nsh], e0) - e0;
                                 const int hi = min(sm.s_off[(jb + 1) * nsh], e1) - e0;
-                                if (lo < hi) apply_rows(sm.L_rs, sm.L_d, sm.L_ph, -1, lo, hi, w2, Wb, Tb, ta);
+                                if (lo < hi) ROWS(sm.L_rs, sm.L_d, sm.L_ph, -1, lo, hi, w2, Wb, Tb, sm.ring, ta);
                                 bar_apply();
                             }
                         }
@@ -876,6 +1279,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 cph = ph0 + (k1 - k0);
                 cit = it0;
                 ++nbatch;
+                t_rows += clock64() - tr0;
             }
             t_busy += clock64() - t0;
             if (stopg >= 0 && C >= stopg) break;
@@ -886,6 +1290,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             prof[6] = (unsigned long long)nbatch;
             prof[10] = (unsigned long long)t_stage;
             prof[11] = (unsigned long long)t_diag;
+            prof[8] = (unsigned long long)t_heads;
+            prof[15] = (unsigned long long)t_rows;
         }
     }
 #undef TD
@@ -904,14 +1310,17 @@ int qblock_rmax(int share, int D) { return share + 2 * (D - 1) + 2; }
 
 size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem) {
     auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
-    const size_t cap = (size_t)qblock_cellcap(share, D);
+    const size_t cap = 2 * (size_t)qblock_cellcap(share, D);  // two cell buffers
     size_t b = 0;
     b += al(sizeof(int2) * qb::kPairCap) + 2 * al(sizeof(double) * qb::kPairCap) + al(sizeof(int) * qb::kPairCap);
     b += al(sizeof(int) * ((size_t)qb::kBatch * nblk + 1));
     b += al(sizeof(unsigned) * (size_t)((p + 31) / 32));
-    b += al(sizeof(int) * cap) + 2 * al(sizeof(double) * cap) + al(sizeof(double) * cap * (qb::kDMax - 1));
+    b += 2 * al(sizeof(int) * cap) + 2 * al(sizeof(double) * cap) + al(sizeof(double) * cap * (qb::kDMax - 1));
     b += al(sizeof(double) * (size_t)qb::kDMax * qblock_rmax(share, D));
     b += al(sizeof(short) * cap * (qb::kDMax - 1));
+    b += al(sizeof(double2) * 2 * (size_t)qb::kApply * qb::kAsyncStages);
+    b += al(sizeof(double) * (size_t)qb::kDMax * share);
+    b += al(sizeof(int2) * (size_t)qb::kBatch * nblk) + al(sizeof(double2) * (size_t)qb::kBatch * nblk);
     if (tdiag_smem) b += al(sizeof(double) * (size_t)p);
     return b;
 }

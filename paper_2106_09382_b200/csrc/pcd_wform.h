@@ -91,6 +91,12 @@ struct WformArgs {
 #ifndef QB_CHAIN_WARPS
 #define QB_CHAIN_WARPS 6     // chain warps of the blocked kernel (the block's cells are loaded in parallel)
 #endif
+#ifndef QB_ASYNC_STAGES
+#define QB_ASYNC_STAGES 6    // per-thread cp.async ring depth of the blocked kernel's row streams (0: registers)
+#endif
+#ifndef QB_ASYNC_HEADS
+#define QB_ASYNC_HEADS 1     // blocked kernel: segment heads copied asynchronously while the apply warps stage
+#endif
 #ifndef QB_DEFAULT_D
 #define QB_DEFAULT_D 4
 #endif
