@@ -116,6 +116,7 @@ struct concord_solver {
     int2* qb_lrs = nullptr;
     double2* qb_ldn = nullptr;
     int* qb_lcnt = nullptr;
+    long long* qb_hang = nullptr;  // mapped host memory: the blocked kernel's watchdog report
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     double* T = nullptr;
@@ -305,6 +306,8 @@ int setup_qblock(concord_solver* s) {
     CK(dalloc(&s->qb_lrs, (size_t)s->qb_rl * s->nblk_tot * s->share));
     CK(dalloc(&s->qb_ldn, (size_t)s->qb_rl * s->nblk_tot * s->share));
     CK(dalloc(&s->qb_lcnt, (size_t)s->qb_rl * s->nblk_tot));
+    CK(cudaHostAlloc((void**)&s->qb_hang, 8 * sizeof(long long), cudaHostAllocMapped));
+    memset(s->qb_hang, 0, 8 * sizeof(long long));
     s->qb = true;
     return CONCORD_OK;
 }
@@ -508,6 +511,7 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->qb_lrs);
     cudaFree(s->qb_ldn);
     cudaFree(s->qb_lcnt);
+    if (s->qb_hang) cudaFreeHost(s->qb_hang);
     for (int r = 0; r < WFORM_MAX_SHARDS; ++r) {
         if (!s->arena[r]) continue;
         if (s->arena_owned[r]) cudaFree(s->arena[r]);
@@ -692,6 +696,9 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.rec_nnz = a.rec_nnz;
         q.status = a.status;
         q.prof = a.prof;
+        long long* hang_d = nullptr;
+        CK(cudaHostGetDevicePointer((void**)&hang_d, s->qb_hang, 0));
+        q.hang = hang_d;
         CK(launch_pcd_qblock(q, s->nblk_launch, s->stream));
     } else {
         CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
@@ -701,9 +708,22 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
 
     int status[2] = {0, 0};
     unsigned long long edges = 0;
-    CK(cudaMemcpyAsync(status, s->status, sizeof(status), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
+    {
+        cudaError_t e = cudaMemcpyAsync(status, s->status, sizeof(status), cudaMemcpyDeviceToHost, s->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+        if (e != cudaSuccess && s->qb && s->qb_hang[0] != 0) {
+            const long long* h = s->qb_hang;
+            static const char* what[3] = {"grid barrier (value, target)", "chain waiting for its stager (block, staged)",
+                                          "apply warps idle (phase, epoch, staged, stop)"};
+            const int k = (int)(h[0] - 1) < 3 ? (int)(h[0] - 1) : 2;
+            return fail(CONCORD_ERR_CUDA,
+                        "fit kernel watchdog (no progress for 20 s): CTA %lld at block %lld, %s = %lld %lld %lld %lld; "
+                        "CUDA: %s",
+                        h[1], h[2], what[k], h[3], h[4], h[5], h[6], cudaGetErrorString(e));
+        }
+        CK(e);
+    }
     const int iters = status[0];
     s->last_iters = iters;
     // every shard ran the same phases: the barrier saw (phases) * nblk_tot arrivals, one per CTA

@@ -362,10 +362,37 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
 #define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) apply_rows(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ta_)
 #endif
 
-__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target) {
+// Watchdog of every spin loop of the kernel: a wait that lasts kHangNs turns into a
+// diagnostic line and a trap (a launch error on the host) instead of a hung device.
+constexpr unsigned long long kHangNs = 20ull * 1000ull * 1000ull * 1000ull;
+
+// The report goes to mapped host memory (readable after the trap): what, CTA, block, values.
+__device__ __forceinline__ void hang_report(long long* hang, int what, int blk, long long v0, long long v1,
+                                            long long v2, long long v3) {
+    volatile long long* h = hang;
+    h[1] = blockIdx.x;
+    h[2] = blk;
+    h[3] = v0;
+    h[4] = v1;
+    h[5] = v2;
+    h[6] = v3;
+    __threadfence_system();
+    h[0] = what + 1;
+    __threadfence_system();
+    __trap();
+}
+
+__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target, int blk,
+                                             long long* hang) {
     unsigned long long v;
+    const unsigned long long t0 = globaltimer_ns();
+    int spins = 0;
     do {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (++spins == 4096) {
+            spins = 0;
+            if (globaltimer_ns() - t0 > kHangNs) hang_report(hang, 0, blk, (long long)v, (long long)target, 0, 0);
+        }
     } while (v < target);
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -634,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const long long t0 = clock64();
             const Blk k = block_at(blk, m, D, NB);
             if (tc == 0) {
-                wait_counter(a.bar, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk);
+                wait_counter(a.bar, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk, blk, a.hang);
                 st_vol(&s_epoch, k.g0);  // deltas and lists of every phase < g0 are visible
                 st_vol(&s_blk, blk);
             }
@@ -876,7 +903,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 // arriving: part A of the next block's cells reads it before that block's barrier
                 if (gt == 0) {
                     const long long tw0 = clock64();
+                    const unsigned long long g0t = globaltimer_ns();
                     while (ld_acquire_cta(&s_staged) < blk + 2) {
+                        if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, blk, blk + 2, ld_vol(&s_staged), 0, 0);
                     }
                     t_c3 += clock64() - tw0;
                     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
@@ -915,6 +944,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         int cit = -1;  // sweep of C
         int staged = 1;  // highest block staged
         long long t_busy = 0, t_idle = 0, nbatch = 0, t_diag = 0, t_stage = 0, t_heads = 0, t_rows = 0;
+        unsigned long long idle_since = 0;  // watchdog (thread ta == 0)
         while (true) {
             const long long t0 = clock64();
             bar_apply();
@@ -950,9 +980,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 3 && Cp <= E - 1 && C >= Cp - a.stage_window;
             if (!have && !can_stage) {
                 t_idle += clock64() - t0;
+                // the chain stopped after this slab already reached the last phase: done
+                if (stopg >= 0 && C >= stopg) break;
+                if (ta == 0) {
+                    if (idle_since == 0) idle_since = globaltimer_ns();
+                    else if (globaltimer_ns() - idle_since > kHangNs) hang_report(a.hang, 2, cblk, C, E, staged, stopg);
+                }
                 __nanosleep(32);
                 continue;
             }
+            idle_since = 0;
 
 #if QB_ASYNC_HEADS
             // ---- segment heads (count + first entry) of the batch's colours: copied

@@ -564,6 +564,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             const int nq = max(0, target - staged);
             if (!have && nq == 0) {
                 t_idle += clock64() - t0;
+                // the chain stopped after this slab already reached the last phase: done
+                if (stopg >= 0 && C >= stopg) break;
                 __nanosleep(32);
                 continue;
             }

@@ -135,6 +135,7 @@ struct QbArgs {
     long long* rec_nnz;
     int* status;
     unsigned long long* prof;
+    long long* hang;       // [8] mapped host memory: watchdog report (what+1, CTA, block, 4 values)
 };
 int qblock_cellcap(int share, int D);
 int qblock_rmax(int share, int D);

@@ -304,3 +304,36 @@ def test_device_check_optimality_and_entries(golden, name, tmp_path):
     fileio.write_estimate(str(path), ents, c["lam"], rep.iterations, rep.final_delta, p=c["p"])
     est, _ = fileio.read_estimate(str(path))
     assert np.array_equal(est.omega, rep.estimate.omega)
+
+
+# ------------------------------------------------- blocked kernel == per-phase kernel
+
+
+@pytest.mark.parametrize("p,lam", [(1000, 0.03), (1000, 0.3), (777, 0.1), (2001, 0.2)])
+def test_blocked_kernel_bitwise_equals_per_phase_kernel(p, lam, monkeypatch):
+    """pcd_qblock.cu (temporally blocked, D colours per barrier) against
+    pcd_wform.cu (one barrier per colour): the same FMAs in the same order, so
+    the same bits, for several D.  lam=0.03 makes most pairs move, so batches
+    hit both row-conflict paths (per-row chains and phase-by-phase passes);
+    odd p exercises the phantom id."""
+    _, t = synth.problem("ar2", p, 400, seed=5)
+    g = cb.GramMatrix(t, 400)
+    def run():
+        with cb.Solver(p) as s:
+            kern = s.layout()["kernel"]
+            s.set_gram(g)
+            rc, res, deltas, objs, _ = s.fit_raw(lam, 1e-5, 30)  # lam=0.03 may not converge: compare anyway
+            return kern, res.iterations, s.omega(), np.array(deltas), np.array(objs)
+
+    monkeypatch.setenv("CONCORD_KERNEL", "wform")
+    k0, it0, om0, dl0, ob0 = run()
+    assert k0 == 0
+    monkeypatch.delenv("CONCORD_KERNEL")
+    for d in ("2", "3", "4", "5"):
+        monkeypatch.setenv("CONCORD_QB_D", d)
+        k, it, om, dl, ob = run()
+        assert k == int(d)
+        assert it == it0, d
+        assert np.array_equal(om, om0), d
+        assert np.array_equal(dl, dl0), d
+        np.testing.assert_allclose(ob, ob0, rtol=1e-12)
