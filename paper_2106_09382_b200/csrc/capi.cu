@@ -116,7 +116,7 @@ struct concord_solver {
     int2* qb_lrs = nullptr;
     double2* qb_ldn = nullptr;
     int* qb_lcnt = nullptr;
-    long long* qb_hang = nullptr;  // mapped host memory: the blocked kernel's watchdog report
+    long long* hang = nullptr;  // mapped host memory: the fit kernels' watchdog report
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     double* T = nullptr;
@@ -306,8 +306,6 @@ int setup_qblock(concord_solver* s) {
     CK(dalloc(&s->qb_lrs, (size_t)s->qb_rl * s->nblk_tot * s->share));
     CK(dalloc(&s->qb_ldn, (size_t)s->qb_rl * s->nblk_tot * s->share));
     CK(dalloc(&s->qb_lcnt, (size_t)s->qb_rl * s->nblk_tot));
-    CK(cudaHostAlloc((void**)&s->qb_hang, 8 * sizeof(long long), cudaHostAllocMapped));
-    memset(s->qb_hang, 0, 8 * sizeof(long long));
     s->qb = true;
     return CONCORD_OK;
 }
@@ -381,6 +379,8 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
     CKC(cudaMemsetAsync(s->T, 0, sizeof(double) * tot, s->stream));
     CKC(cudaMemsetAsync(s->W, 0, sizeof(double) * tot, s->stream));
     CKC(cudaMemsetAsync(s->Om, 0, sizeof(double) * tot, s->stream));
+    CKC(cudaHostAlloc((void**)&s->hang, 8 * sizeof(long long), cudaHostAllocMapped));
+    memset(s->hang, 0, 8 * sizeof(long long));
     CKC(dalloc(&s->tdiag, ip));
     CKC(dalloc(&s->diagd, (size_t)s->nblk_launch * ip));
     {
@@ -511,13 +511,13 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->qb_lrs);
     cudaFree(s->qb_ldn);
     cudaFree(s->qb_lcnt);
-    if (s->qb_hang) cudaFreeHost(s->qb_hang);
     for (int r = 0; r < WFORM_MAX_SHARDS; ++r) {
         if (!s->arena[r]) continue;
         if (s->arena_owned[r]) cudaFree(s->arena[r]);
         else cudaIpcCloseMemHandle(s->arena[r]);
     }
     cudaFree(s->edges);
+    if (s->hang) cudaFreeHost(s->hang);
     cudaFree(s->status);
     cudaFree(s->rec_delta);
     cudaFree(s->rec_obj);
@@ -629,6 +629,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     a.delta_tol = prm->delta_tol;
     a.max_iter = prm->max_iter;
     a.want_trace = prm->want_trace ? 1 : 0;
+    CK(cudaHostGetDevicePointer((void**)&a.hang, s->hang, 0));
     a.lmax = s->lmax;
     a.rd = s->rd;
     a.rl = s->rl;
@@ -696,9 +697,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.rec_nnz = a.rec_nnz;
         q.status = a.status;
         q.prof = a.prof;
-        long long* hang_d = nullptr;
-        CK(cudaHostGetDevicePointer((void**)&hang_d, s->qb_hang, 0));
-        q.hang = hang_d;
+        q.hang = a.hang;
         CK(launch_pcd_qblock(q, s->nblk_launch, s->stream));
     } else {
         CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
@@ -712,13 +711,13 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         cudaError_t e = cudaMemcpyAsync(status, s->status, sizeof(status), cudaMemcpyDeviceToHost, s->stream);
         if (e == cudaSuccess) e = cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-        if (e != cudaSuccess && s->qb && s->qb_hang[0] != 0) {
-            const long long* h = s->qb_hang;
+        if (e != cudaSuccess && s->hang && s->hang[0] != 0) {
+            const long long* h = s->hang;
             static const char* what[3] = {"grid barrier (value, target)", "chain waiting for its stager (block, staged)",
                                           "apply warps idle (phase, epoch, staged, stop)"};
             const int k = (int)(h[0] - 1) < 3 ? (int)(h[0] - 1) : 2;
             return fail(CONCORD_ERR_CUDA,
-                        "fit kernel watchdog (no progress for 20 s): CTA %lld at block %lld, %s = %lld %lld %lld %lld; "
+                        "fit kernel watchdog (no progress for 20 s): CTA %lld at block/phase %lld, %s = %lld %lld %lld %lld; "
                         "CUDA: %s",
                         h[1], h[2], what[k], h[3], h[4], h[5], h[6], cudaGetErrorString(e));
         }

@@ -123,6 +123,27 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
+// Watchdog of every spin loop of the fit kernels: a wait that lasts kHangNs turns into a
+// diagnostic line and a trap (a launch error on the host) instead of a hung device.
+constexpr unsigned long long kHangNs = 20ull * 1000ull * 1000ull * 1000ull;
+
+// The report goes to mapped host memory (readable after the trap): what, CTA, block, values.
+__device__ __forceinline__ void hang_report(long long* hang, int what, int blk, long long v0, long long v1,
+                                            long long v2, long long v3) {
+    volatile long long* h = hang;
+    h[1] = blockIdx.x;
+    h[2] = blk;
+    h[3] = v0;
+    h[4] = v1;
+    h[5] = v2;
+    h[6] = v3;
+    __threadfence_system();
+    h[0] = what + 1;
+    __threadfence_system();
+    __trap();
+}
+
+
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 
 template <typename T>

@@ -186,10 +186,17 @@ __device__ __forceinline__ void arrive_all(const WformArgs& a) {
 
 // Wait until the barrier counter reaches `target`: relaxed polling (a plain L2
 // load per iteration, no L1 invalidate per poll), then one acquire fence.
-__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target, int sys) {
+__device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target, int sys,
+                                             int g, long long* hang) {
     unsigned long long v;
+    const unsigned long long t0 = globaltimer_ns();
+    int spins = 0;
     do {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (++spins == 4096) {
+            spins = 0;
+            if (globaltimer_ns() - t0 > kHangNs) hang_report(hang, 0, g, (long long)v, (long long)target, 0, 0);
+        }
     } while (v < target);
     if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
     else asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             long long t0 = clock64();
             if (tc == 0) {
                 const unsigned long long target = a.bar_base + (unsigned long long)(g + 1) * (unsigned long long)nblk;
-                wait_counter(barL, target, a.sys_scope);
+                wait_counter(barL, target, a.sys_scope, g, a.hang);
                 st_vol(&s_epoch, g);
             }
             bar_chain();
@@ -383,7 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 const int phQ = (ph == m) ? 0 : ph + 1;
                 const int slot = Q % kSlots;
                 if (tc < wl) {
+                    const unsigned long long g0t = globaltimer_ns();
                     while (ld_acquire_cta(&s_staged) < Q) {
+                        if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, g, Q, ld_vol(&s_staged), 0, 0);
                     }
                 }
                 long long t2 = clock64();
@@ -535,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         int cit = -1;          // sweep of C
         int staged = init_hi;  // highest publish phase staged
         long long t_busy = 0, t_idle = 0, nbatch = 0, t_head = 0, t_diag = 0, t_h0 = 0, t_h1 = 0, t_h2 = 0;
+        unsigned long long idle_since = 0;  // watchdog (thread ta == 0)
         while (true) {
             const long long t0 = clock64();
             bar_apply();  // everyone has consumed the previous broadcast
@@ -566,9 +576,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 t_idle += clock64() - t0;
                 // the chain stopped after this slab already reached the last phase: done
                 if (stopg >= 0 && C >= stopg) break;
+                if (ta == 0) {
+                    if (idle_since == 0) idle_since = globaltimer_ns();
+                    else if (globaltimer_ns() - idle_since > kHangNs) hang_report(a.hang, 2, E, C, E, staged, stopg);
+                }
                 __nanosleep(32);
                 continue;
             }
+            idle_since = 0;
 
             const long long ta0 = clock64();
             // ---- one round trip: segment heads (count + first entry) and the stage cells

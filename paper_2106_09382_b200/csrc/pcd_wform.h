@@ -79,6 +79,7 @@ struct WformArgs {
     int tdiag_smem;                 // 1: the T diagonal is copied into shared memory
     int* status;                    // [0] iterations, [1] converged
     unsigned long long* prof;       // optional [16] cycle counters (CTA 0), or NULL
+    long long* hang;  // [8] mapped host memory: watchdog report (what+1, CTA, phase/block, 4 values)
 };
 
 // Temporally blocked variant (pcd_qblock.cu): D colour phases per grid barrier.
