@@ -382,29 +382,54 @@ struct Layout {
     int ncell, rd0, ph0w, rdb, phb;
 };
 
+// Dynamic shared memory of the blocked kernel, addressed by 32-bit offsets from one
+// shared base (one register per array, native shared addressing) instead of generic pointers.
+extern __shared__ __align__(16) unsigned char qb_smem[];
+
 struct Smem {
-    int2* L_rs;     // [kPairCap]  delta-list chunk
-    double* L_d;    // [kPairCap]
-    double* L_new;  // [kPairCap]
-    int* L_ph;      // [kPairCap]
-    int* s_off;     // [kBatch * nblk + 1]
-    unsigned* bm;   // [(p + 31) / 32]
-    double* td;     // [p] T diagonal, or NULL
-    int* cX;        // [cellcap] row of each block cell (-1: phantom)
-    int* cC;        // [cellcap] column of each block cell
-    double* cW;     // [cellcap] cell value brought forward to the start of the block
-    double* cO;     // [cellcap] Omega of the cell
-    double* cT;     // [cellcap][kDMax-1] T entries of the block's earlier phases
-    double* sd;     // [kDMax][rmax] delta of each pair of the block's phases (extended ranges)
-    short* cQ;      // [cellcap][kDMax-1] index into sd[i] of the cell row's pair at in-block phase i
-    double* snv;    // [kDMax][share] new value of each own pair of the block's colours
-    int2* hd_rs;    // [kBatch * nblk] first entry of each list segment of a batch
-    double2* hd_dn; // [kBatch * nblk]
-    double2* ring;  // [kAsyncStages][2][kApply] per-thread cp.async slots of the row streams
+    unsigned o_L_rs;  // [kPairCap]  delta-list chunk
+    unsigned o_L_d;  // [kPairCap]
+    unsigned o_L_new;  // [kPairCap]
+    unsigned o_L_ph;  // [kPairCap]
+    unsigned o_s_off;  // [kBatch * nblk + 1]
+    unsigned o_bm;  // [(p + 31) / 32]
+    unsigned o_td;  // [p] T diagonal, or NULL
+    unsigned o_cX;  // [cellcap] row of each block cell (-1: phantom)
+    unsigned o_cC;  // [cellcap] column of each block cell
+    unsigned o_cW;  // [cellcap] cell value brought forward to the start of the block
+    unsigned o_cO;  // [cellcap] Omega of the cell
+    unsigned o_cT;  // [cellcap][kDMax-1] T entries of the block's earlier phases
+    unsigned o_sd;  // [kDMax][rmax] delta of each pair of the block's phases (extended ranges)
+    unsigned o_cQ;  // [cellcap][kDMax-1] index into sd[i] of the cell row's pair at in-block phase i
+    unsigned o_snv;  // [kDMax][share] new value of each own pair of the block's colours
+    unsigned o_hd_rs;  // [kBatch * nblk] first entry of each list segment of a batch
+    unsigned o_hd_dn;  // [kBatch * nblk]
+    unsigned o_ring;  // [kAsyncStages][2][kApply] per-thread cp.async slots of the row streams
+    __device__ __forceinline__ int2* L_rs() const { return reinterpret_cast<int2*>(qb_smem + o_L_rs); }
+    __device__ __forceinline__ double* L_d() const { return reinterpret_cast<double*>(qb_smem + o_L_d); }
+    __device__ __forceinline__ double* L_new() const { return reinterpret_cast<double*>(qb_smem + o_L_new); }
+    __device__ __forceinline__ int* L_ph() const { return reinterpret_cast<int*>(qb_smem + o_L_ph); }
+    __device__ __forceinline__ int* s_off() const { return reinterpret_cast<int*>(qb_smem + o_s_off); }
+    __device__ __forceinline__ unsigned* bm() const { return reinterpret_cast<unsigned*>(qb_smem + o_bm); }
+    __device__ __forceinline__ double* td() const { return reinterpret_cast<double*>(qb_smem + o_td); }
+    __device__ __forceinline__ int* cX() const { return reinterpret_cast<int*>(qb_smem + o_cX); }
+    __device__ __forceinline__ int* cC() const { return reinterpret_cast<int*>(qb_smem + o_cC); }
+    __device__ __forceinline__ double* cW() const { return reinterpret_cast<double*>(qb_smem + o_cW); }
+    __device__ __forceinline__ double* cO() const { return reinterpret_cast<double*>(qb_smem + o_cO); }
+    __device__ __forceinline__ double* cT() const { return reinterpret_cast<double*>(qb_smem + o_cT); }
+    __device__ __forceinline__ double* sd() const { return reinterpret_cast<double*>(qb_smem + o_sd); }
+    __device__ __forceinline__ short* cQ() const { return reinterpret_cast<short*>(qb_smem + o_cQ); }
+    __device__ __forceinline__ double* snv() const { return reinterpret_cast<double*>(qb_smem + o_snv); }
+    __device__ __forceinline__ int2* hd_rs() const { return reinterpret_cast<int2*>(qb_smem + o_hd_rs); }
+    __device__ __forceinline__ double2* hd_dn() const { return reinterpret_cast<double2*>(qb_smem + o_hd_dn); }
+    __device__ __forceinline__ double2* ring() const { return reinterpret_cast<double2*>(qb_smem + o_ring); }
 };
 
+// kProf: the phase profiler (CONCORD_PHASE_PROFILE); the production instantiation carries
+// no timers at all (they would hold ~30 registers across the loops).
+template <bool kProf>
+#define PCLK() (kProf ? clock64() : 0ll)
 __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_epoch, s_blk, s_stop, s_staged, s_iters, s_conv;
     __shared__ int s_cnt[kDMax];
     __shared__ short s_next[2 * kChainN];
@@ -430,35 +455,35 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
 
     Smem sm;
     {
-        unsigned char* ptr = smem_raw;
+        unsigned off = 0;
         auto take = [&](size_t bytes) {
-            unsigned char* r = ptr;
-            ptr += (bytes + 15) & ~(size_t)15;
+            const unsigned r = off;
+            off += (unsigned)((bytes + 15) & ~(size_t)15);
             return r;
         };
-        sm.L_rs = reinterpret_cast<int2*>(take(sizeof(int2) * kPairCap));
-        sm.L_d = reinterpret_cast<double*>(take(sizeof(double) * kPairCap));
-        sm.L_new = reinterpret_cast<double*>(take(sizeof(double) * kPairCap));
-        sm.L_ph = reinterpret_cast<int*>(take(sizeof(int) * kPairCap));
-        sm.s_off = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)kBatch * nblk + 1)));
-        sm.bm = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (size_t)((p + 31) / 32)));
-        sm.cX = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)a.cellcap));
-        sm.cC = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)a.cellcap));
-        sm.cW = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)a.cellcap));
-        sm.cO = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)a.cellcap));
-        sm.cT = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)a.cellcap * (kDMax - 1)));
-        sm.sd = reinterpret_cast<double*>(take(sizeof(double) * (size_t)kDMax * a.rmax));
-        sm.cQ = reinterpret_cast<short*>(take(sizeof(short) * 2 * (size_t)a.cellcap * (kDMax - 1)));
-        sm.snv = reinterpret_cast<double*>(take(sizeof(double) * (size_t)kDMax * a.share));
-        sm.hd_rs = reinterpret_cast<int2*>(take(sizeof(int2) * (size_t)kBatch * nblk));
-        sm.hd_dn = reinterpret_cast<double2*>(take(sizeof(double2) * (size_t)kBatch * nblk));
-        sm.ring = kAsyncStages ? reinterpret_cast<double2*>(take(sizeof(double2) * 2 * (size_t)kApply * kAsyncStages)) : nullptr;
-        sm.td = a.tdiag_smem ? reinterpret_cast<double*>(take(sizeof(double) * (size_t)p)) : nullptr;
+        sm.o_L_rs = take(sizeof(int2) * kPairCap);
+        sm.o_L_d = take(sizeof(double) * kPairCap);
+        sm.o_L_new = take(sizeof(double) * kPairCap);
+        sm.o_L_ph = take(sizeof(int) * kPairCap);
+        sm.o_s_off = take(sizeof(int) * ((size_t)kBatch * nblk + 1));
+        sm.o_bm = take(sizeof(unsigned) * (size_t)((p + 31) / 32));
+        sm.o_cX = take(sizeof(int) * 2 * (size_t)a.cellcap);
+        sm.o_cC = take(sizeof(int) * 2 * (size_t)a.cellcap);
+        sm.o_cW = take(sizeof(double) * 2 * (size_t)a.cellcap);
+        sm.o_cO = take(sizeof(double) * 2 * (size_t)a.cellcap);
+        sm.o_cT = take(sizeof(double) * 2 * (size_t)a.cellcap * (kDMax - 1));
+        sm.o_sd = take(sizeof(double) * (size_t)kDMax * a.rmax);
+        sm.o_cQ = take(sizeof(short) * 2 * (size_t)a.cellcap * (kDMax - 1));
+        sm.o_snv = take(sizeof(double) * (size_t)kDMax * a.share);
+        sm.o_hd_rs = take(sizeof(int2) * (size_t)kBatch * nblk);
+        sm.o_hd_dn = take(sizeof(double2) * (size_t)kBatch * nblk);
+        sm.o_ring = kAsyncStages ? take(sizeof(double2) * 2 * (size_t)kApply * kAsyncStages) : 0xffffffffu;
+        sm.o_td = a.tdiag_smem ? take(sizeof(double) * (size_t)p) : 0xffffffffu;
     }
-    if (sm.td)
-        for (int i = tid; i < p; i += kThreads) sm.td[i] = __ldg(a.tdiag + i);
-    for (int i = tid; i < (p + 31) / 32; i += kThreads) sm.bm[i] = 0u;
-#define TD(i) (sm.td ? sm.td[i] : __ldg(a.tdiag + (i)))
+    if (a.tdiag_smem)
+        for (int i = tid; i < p; i += kThreads) sm.td()[i] = __ldg(a.tdiag + i);
+    for (int i = tid; i < (p + 31) / 32; i += kThreads) sm.bm()[i] = 0u;
+#define TD(i) (a.tdiag_smem ? sm.td()[i] : __ldg(a.tdiag + (i)))
 
     // ---- stage blocks 0 and 1 from the initial W, Omega (watermark -1)
     for (int bb = 0; bb < 2 && bb < 2 * NB; ++bb) {
@@ -488,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     }
     __syncthreads();
 
-    unsigned long long* prof = (a.prof && b == 0) ? a.prof : nullptr;
+    unsigned long long* prof = (kProf && a.prof && b == 0) ? a.prof : nullptr;
 
     if (warp < kChainWarps) {
         // ================================================================ chain warps
@@ -566,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     int r, s2;
                     round_pair(q, m, m - 1 - (kB.ph0 + d), r, s2);
                     if (s2 >= p) {
-                        sm.cX[cb + ci] = -1;
+                        sm.cX()[cb + ci] = -1;
                         continue;
                     }
                     x = (rel & 1) ? s2 : r;
@@ -579,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     round_pair(q, m, 0, r, s2);  // colour m-1
                     x = (rel & 1) ? s2 : r;
                     if (x >= p) {
-                        sm.cX[cb + ci] = -1;
+                        sm.cX()[cb + ci] = -1;
                         continue;
                     }
                     c = x;
@@ -599,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     int pos = (x == 0) ? 0 : 1 + (x - 1 + kB.ph0) % m;
                     for (int i = 0; i < d; ++i) {
                         const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
-                        sm.cQ[(size_t)(cb + ci) * (kDMax - 1) + i] = (short)(qi - L.lo[i]);
+                        sm.cQ()[(size_t)(cb + ci) * (kDMax - 1) + i] = (short)(qi - L.lo[i]);
                         if (x != 0) pos = (pos == m) ? 1 : pos + 1;
                     }
                 }
@@ -628,17 +653,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     for (int u = 0; u < 2 * kDMax; ++u)
                         if (mask & (1u << u)) val = fma(dj[u], tj[u], val);
                 }
-                sm.cX[cb + ci] = x;
-                sm.cC[cb + ci] = c;
-                sm.cW[cb + ci] = val;
-                sm.cO[cb + ci] = om;
+                sm.cX()[cb + ci] = x;
+                sm.cC()[cb + ci] = c;
+                sm.cW()[cb + ci] = val;
+                sm.cO()[cb + ci] = om;
 #pragma unroll
-                for (int i = 0; i < kDMax - 1; ++i) sm.cT[(size_t)(cb + ci) * (kDMax - 1) + i] = tin[i];
+                for (int i = 0; i < kDMax - 1; ++i) sm.cT()[(size_t)(cb + ci) * (kDMax - 1) + i] = tin[i];
             }
         };
         int blk = 0;
         while (true) {
-            const long long t0 = clock64();
+            const long long t0 = PCLK();
             const Blk k = block_at(blk, m, D, NB);
             if (tc == 0) {
                 wait_counter(a.bar, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk, blk, a.hang);
@@ -646,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 st_vol(&s_blk, blk);
             }
             bar_chain();
-            const long long t1 = clock64();
+            const long long t1 = PCLK();
             t_wait += t1 - t0;
             // ---- the previous block closed a sweep: convergence decision (identical in every CTA)
             if (k.ph0 == 0 && blk > 0) {
@@ -683,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const int nbv = k.g0 - hiA;
                 const int ntotB = L.ncell + (has_diag ? 2 * (q_hi - q_lo) : 0);
                 for (int ci = tc; ci < ntotB; ci += kChain) {
-                    const int x = sm.cX[cb + ci];
+                    const int x = sm.cX()[cb + ci];
                     if (x < 0) continue;
                     double dj[kDMax];
                     int slot = L.rdb;
@@ -697,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     for (int u = 0; u < kDMax; ++u)
                         if (dj[u] != 0.0) mask |= 1u << u;
                     if (mask) {
-                        const int c = sm.cC[cb + ci];
+                        const int c = sm.cC()[cb + ci];
                         const int cs = c / w;  // slab of column c
                         const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
                         double tj[kDMax];
@@ -707,18 +732,18 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             tj[u] = ldcg_if(Tc + (long long)pw.y() * w, (mask >> u) & 1u);
                             pw.next();
                         }
-                        double val = sm.cW[cb + ci];
+                        double val = sm.cW()[cb + ci];
 #pragma unroll
                         for (int u = 0; u < kDMax; ++u)
                             if (mask & (1u << u)) val = fma(dj[u], tj[u], val);
-                        sm.cW[cb + ci] = val;
+                        sm.cW()[cb + ci] = val;
                     }
                 }
             }
             bar_chain();
             const int ncell = L.ncell;
             const int ndiag = has_diag ? 2 * (q_hi - q_lo) : 0;
-            const long long t2 = clock64();
+            const long long t2 = PCLK();
             t_load += t2 - t1;
 
             if (in_cg) {
@@ -731,13 +756,13 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const int hi = min(half, q_hi + h);
                     const int lod = L.lo[d], cbd = cb + L.cb[d];
                     const int c1 = m - 1 - ph;
-                    double* sdd = sm.sd + (size_t)d * a.rmax;
+                    double* sdd = sm.sd() + (size_t)d * a.rmax;
                     const int sid = ng - 1 - gt;
                     for (int base = lod; base < hi; base += ng) {
                         const int q = base + sid;
                         if (q >= hi) continue;
                         long long tp0 = 0, tp1 = 0, tp2 = 0;
-                        if (prof && sid == 0) tp0 = clock64();
+                        if (prof && sid == 0) tp0 = PCLK();
                         int r, s;
                         round_pair(q, m, c1, r, s);
                         double dl = 0.0, nv = 0.0;
@@ -750,17 +775,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             double di[2][kDMax - 1], ti[2][kDMax - 1], v2[2];
 #pragma unroll
                             for (int side = 0; side < 2; ++side) {
-                                v2[side] = sm.cW[ci + side];
+                                v2[side] = sm.cW()[ci + side];
 #pragma unroll
                                 for (int i = 0; i < kDMax - 1; ++i)
-                                    qi[side][i] = (i < d) ? sm.cQ[(size_t)(ci + side) * (kDMax - 1) + i] : (short)0;
+                                    qi[side][i] = (i < d) ? sm.cQ()[(size_t)(ci + side) * (kDMax - 1) + i] : (short)0;
                             }
 #pragma unroll
                             for (int side = 0; side < 2; ++side)
 #pragma unroll
                                 for (int i = 0; i < kDMax - 1; ++i) {
-                                    di[side][i] = (i < d) ? sm.sd[(size_t)i * a.rmax + qi[side][i]] : 0.0;
-                                    ti[side][i] = (i < d) ? sm.cT[(size_t)(ci + side) * (kDMax - 1) + i] : 0.0;
+                                    di[side][i] = (i < d) ? sm.sd()[(size_t)i * a.rmax + qi[side][i]] : 0.0;
+                                    ti[side][i] = (i < d) ? sm.cT()[(size_t)(ci + side) * (kDMax - 1) + i] : 0.0;
                                 }
 #pragma unroll
                             for (int side = 0; side < 2; ++side)
@@ -768,16 +793,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 for (int i = 0; i < kDMax - 1; ++i)
                                     if (i < d && di[side][i] != 0.0) v2[side] = fma(di[side][i], ti[side][i], v2[side]);
                             // side 0: cell (r, s) = W[r,s]; side 1: cell (s, r) = W[s,r]
-                            const double om = sm.cO[ci];
+                            const double om = sm.cO()[ci];
                             if (prof && sid == 0) tp1 = clock_after(v2[0] + v2[1]);
                             dl = pair_delta(make_double2(v2[1], om), make_double2(v2[0], om), TD(r), TD(s), a.shrink,
                                             nv);
                             if (prof && sid == 0) tp2 = clock_after(dl);
                         }
                         sdd[q - lod] = dl;
-                        if (q >= q_lo && q < q_hi) sm.snv[d * a.share + (q - q_lo)] = nv;
+                        if (q >= q_lo && q < q_hi) sm.snv()[d * a.share + (q - q_lo)] = nv;
                         if (prof && sid == 0 && tp2 != 0) {
-                            const long long tp3 = clock64();
+                            const long long tp3 = PCLK();
                             t_q0 += tp1 - tp0;
                             t_q1 += tp2 - tp1;
                             t_q2 += tp3 - tp2;
@@ -797,8 +822,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             d = idx / nown;
                             q = q_lo + (idx - d * nown);
                             round_pair(q, m, m - 1 - (k.ph0 + d), r, s);
-                            dl = sm.sd[(size_t)d * a.rmax + (q - L.lo[d])];
-                            nv = sm.snv[d * a.share + (q - q_lo)];
+                            dl = sm.sd()[(size_t)d * a.rmax + (q - L.lo[d])];
+                            nv = sm.snv()[d * a.share + (q - q_lo)];
                             const size_t dgo = (size_t)L.rdc[d] * p;
                             a.dring[dgo + r] = dl;  // 0 when the partner is the phantom (odd p)
                             if (s < p) a.dring[dgo + s] = dl;
@@ -843,14 +868,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     double dm = 0.0;
                     for (int e = gt; e < ndiag; e += ng) {
                         const int cc = cb + ncell + e;
-                        const int x = sm.cX[cc];
+                        const int x = sm.cX()[cc];
                         if (x < 0) continue;
-                        double val = sm.cW[cc];
+                        double val = sm.cW()[cc];
                         for (int i = 0; i < nbc; ++i) {
-                            const double di = sm.sd[(size_t)i * a.rmax + sm.cQ[(size_t)cc * (kDMax - 1) + i]];
-                            if (di != 0.0) val = fma(di, sm.cT[(size_t)cc * (kDMax - 1) + i], val);
+                            const double di = sm.sd()[(size_t)i * a.rmax + sm.cQ()[(size_t)cc * (kDMax - 1) + i]];
+                            if (di != 0.0) val = fma(di, sm.cT()[(size_t)cc * (kDMax - 1) + i], val);
                         }
-                        const double om = sm.cO[cc];
+                        const double om = sm.cO()[cc];
                         const double nv = diag_from_dot(val, om, TD(x), a.n);
                         const double dl = __dsub_rn(nv, om);
                         a.dring[dgo + x] = dl;
@@ -878,25 +903,25 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + k.sweep), (unsigned long long)nbk);
                     }
                 }
-                if (gt == 0) t_work += clock64() - t2;
+                if (gt == 0) t_work += PCLK() - t2;
                 // ---- the block after next must be staged (by this CTA's apply warps) before
                 // arriving: part A of the next block's cells reads it before that block's barrier
                 if (gt == 0) {
-                    const long long tw0 = clock64();
+                    const long long tw0 = PCLK();
                     const unsigned long long g0t = globaltimer_ns();
                     while (ld_acquire_cta(&s_staged) < blk + 2) {
                         if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, blk, blk + 2, ld_vol(&s_staged), 0, 0);
                     }
-                    t_c3 += clock64() - tw0;
+                    t_c3 += PCLK() - tw0;
                     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
                 }
             }
             // ---- part A of the next block's cells: the prefetch group, concurrently with the
             // colours (or every chain warp, after the arrive)
             if (overlap ? !in_cg : true) {
-                const long long ta0 = clock64();
+                const long long ta0 = PCLK();
                 cells_a(blk + 1, overlap ? cg0 : kChain, overlap ? 4 : 1);
-                t_c0 += clock64() - ta0;
+                t_c0 += PCLK() - ta0;
             }
             bar_chain();
             ++blk;
@@ -926,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         long long t_busy = 0, t_idle = 0, nbatch = 0, t_diag = 0, t_stage = 0, t_heads = 0, t_rows = 0;
         unsigned long long idle_since = 0;  // watchdog (thread ta == 0)
         while (true) {
-            const long long t0 = clock64();
+            const long long t0 = PCLK();
             bar_apply();
             if (ta == 0) {
                 s_aE = ld_vol(&s_epoch);
@@ -938,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 __threadfence_block();
             }
             bar_apply();
-            const long long th0 = clock64();
+            const long long th0 = PCLK();
             const int E = s_aE;
             const int cblk = s_aBlk;
             const int stopg = s_aStop;
@@ -959,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const int Cp = stage_mark(sb, m, D, NB);
             const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 3 && Cp <= E - 1 && C >= Cp - a.stage_window;
             if (!have && !can_stage) {
-                t_idle += clock64() - t0;
+                t_idle += PCLK() - t0;
                 // the chain stopped after this slab already reached the last phase: done
                 if (stopg >= 0 && C >= stopg) break;
                 if (ta == 0) {
@@ -979,15 +1004,15 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const int jb = idx / nsh;
                 const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                 (unsigned)__cvta_generic_to_shared(sm.s_off + idx)),
+                                 (unsigned)__cvta_generic_to_shared(sm.s_off() + idx)),
                              "l"(lcntL + seg)
                              : "memory");
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                                 (unsigned)__cvta_generic_to_shared(sm.hd_rs + idx)),
+                                 (unsigned)__cvta_generic_to_shared(sm.hd_rs() + idx)),
                              "l"(lrsL + (size_t)seg * a.share)
                              : "memory");
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                 (unsigned)__cvta_generic_to_shared(sm.hd_dn + idx)),
+                                 (unsigned)__cvta_generic_to_shared(sm.hd_dn() + idx)),
                              "l"(ldnL + (size_t)seg * a.share)
                              : "memory");
             }
@@ -1000,14 +1025,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const int cnt = __ldcg(lcntL + seg);
                 const int2 rs = __ldcg(lrsL + (size_t)seg * a.share);
                 const double2 dn = __ldcg(ldnL + (size_t)seg * a.share);
-                sm.s_off[idx] = cnt;
+                sm.s_off()[idx] = cnt;
                 if (cnt > 1) s_multi = 1;
                 if (cnt == 1) {
                     const int pos = atomicAdd(&s_nent, 1);
                     if (pos < kPairCap) {
-                        sm.L_rs[pos] = rs;
-                        sm.L_d[pos] = dn.x;
-                        sm.L_ph[pos] = jb;
+                        sm.L_rs()[pos] = rs;
+                        sm.L_d()[pos] = dn.x;
+                        sm.L_ph()[pos] = jb;
                     } else {
                         s_multi = 1;
                     }
@@ -1018,7 +1043,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
 #endif
             // ---- stage block sb: cells brought forward from this slab's watermark C to C'
             if (can_stage) {
-                const long long ts = clock64();
+                const long long ts = PCLK();
                 const Blk kb = block_at(sb, m, D, NB);
                 for (int idx = ta; idx < kb.len * wl; idx += kApply) {
                     const int i = idx / wl, j = idx - i * wl;
@@ -1074,22 +1099,22 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         }
                     }
                 }
-                t_stage += clock64() - ts;
+                t_stage += PCLK() - ts;
             }
 #if QB_ASYNC_HEADS
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             for (int idx = ta; idx < nseg; idx += kApply) {
                 const int jb = idx / nsh;
-                const int cnt = sm.s_off[idx];
+                const int cnt = sm.s_off()[idx];
                 if (cnt > 1) s_multi = 1;
                 if (cnt == 1) {
-                    const int2 rs = sm.hd_rs[idx];
-                    const double2 dn = sm.hd_dn[idx];
+                    const int2 rs = sm.hd_rs()[idx];
+                    const double2 dn = sm.hd_dn()[idx];
                     const int pos = atomicAdd(&s_nent, 1);
                     if (pos < kPairCap) {
-                        sm.L_rs[pos] = rs;
-                        sm.L_d[pos] = dn.x;
-                        sm.L_ph[pos] = jb;
+                        sm.L_rs()[pos] = rs;
+                        sm.L_d()[pos] = dn.x;
+                        sm.L_ph()[pos] = jb;
                     } else {
                         s_multi = 1;
                     }
@@ -1099,7 +1124,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             }
 #endif
             bar_apply();
-            const long long th1 = clock64();
+            const long long th1 = PCLK();
             if (can_stage) {
                 staged = sb;
                 if (ta == 0) {
@@ -1116,8 +1141,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const int iend = min(i0 + kPairCap, p);
                     for (int i = i0 + ta; i < iend; i += kApply) {
                         const double2 v = ldcg2(dd + i);
-                        sm.L_d[i - i0] = v.x;
-                        sm.L_new[i - i0] = v.y;
+                        sm.L_d()[i - i0] = v.x;
+                        sm.L_new()[i - i0] = v.y;
                     }
                     bar_apply();
                     const int items = (iend - i0) * w2;
@@ -1131,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 const int j2 = idx - ii * w2;
                                 const long long off = (long long)(i0 + ii) * w + 2 * j2;
                                 wv[u] = __ldcg(reinterpret_cast<const double2*>(Wb + off));
-                                if (sm.L_d[ii] != 0.0) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + off));
+                                if (sm.L_d()[ii] != 0.0) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + off));
                                 if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
                             }
                         }
@@ -1143,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 const int j2 = idx - ii * w2;
                                 const int i = i0 + ii;
                                 const long long off = (long long)i * w + 2 * j2;
-                                const double d = sm.L_d[ii];
+                                const double d = sm.L_d()[ii];
                                 if (d != 0.0) {
                                     wv[u].x = fma(d, tv[u].x, wv[u].x);
                                     wv[u].y = fma(d, tv[u].y, wv[u].y);
@@ -1153,17 +1178,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 const bool dg0 = (cj == i), dg1 = (cj + 1 == i);
                                 if (a.want_trace) {
                                     if (dg0 | dg1) {
-                                        if (dg0) ov[u].x = sm.L_new[ii];
-                                        if (dg1) ov[u].y = sm.L_new[ii];
+                                        if (dg0) ov[u].x = sm.L_new()[ii];
+                                        if (dg1) ov[u].y = sm.L_new()[ii];
                                         *reinterpret_cast<double2*>(Ob + off) = ov[u];
-                                        log_acc += log(sm.L_new[ii]);
+                                        log_acc += log(sm.L_new()[ii]);
                                     }
                                     q_acc = fma(wv[u].x, ov[u].x, q_acc);
                                     q_acc = fma(wv[u].y, ov[u].y, q_acc);
                                     if (i < cj) pen_acc += fabs(ov[u].x);
                                     if (i < cj + 1) pen_acc += fabs(ov[u].y);
                                 } else if (dg0 | dg1) {
-                                    Ob[off + (dg0 ? 0 : 1)] = sm.L_new[ii];
+                                    Ob[off + (dg0 ? 0 : 1)] = sm.L_new()[ii];
                                 }
                             }
                         }
@@ -1197,95 +1222,95 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 C = k0;
                 cph = m;
                 cit = it0;
-                t_diag += clock64() - t0;
+                t_diag += PCLK() - t0;
             } else if (nb > 0) {
                 // ---- colour phases k0 .. k1
                 t_heads += th1 - th0;
-                const long long tr0 = clock64();
+                const long long tr0 = PCLK();
                 int total = 0;
                 if (!s_multi) {
                     // every segment had at most one entry: they are already in shared memory
                     const int nent = s_nent;
                     if (nb > 1) {
                         for (int e = ta; e < nent; e += kApply) {
-                            const int2 rs = sm.L_rs[e];
+                            const int2 rs = sm.L_rs()[e];
                             const unsigned br = 1u << (rs.x & 31), bs = 1u << (rs.y & 31);
-                            const unsigned o1 = atomicOr(sm.bm + (rs.x >> 5), br);
-                            const unsigned o2 = atomicOr(sm.bm + (rs.y >> 5), bs);
+                            const unsigned o1 = atomicOr(sm.bm() + (rs.x >> 5), br);
+                            const unsigned o2 = atomicOr(sm.bm() + (rs.y >> 5), bs);
                             if ((o1 & br) | (o2 & bs)) s_conflict = 1;
                         }
                         bar_apply();
                     }
                     if (!s_conflict) {
-                        ROWS(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, nent, w2, Wb, Tb, sm.ring, ta);
+                        ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, 0, nent, w2, Wb, Tb, sm.ring(), ta);
                     } else if (nent <= kChainN) {
-                        apply_chains(sm.L_rs, sm.L_d, sm.L_ph, nent, w2, Wb, Tb, s_next, s_first, ta);
+                        apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), nent, w2, Wb, Tb, s_next, s_first, ta);
                     } else {
                         for (int jb = 0; jb < nb; ++jb) {  // rows repeat across phases: phase by phase
-                            ROWS(sm.L_rs, sm.L_d, sm.L_ph, jb, 0, nent, w2, Wb, Tb, sm.ring, ta);
+                            ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), jb, 0, nent, w2, Wb, Tb, sm.ring(), ta);
                             bar_apply();
                         }
                     }
                     bar_apply();
                     if (nb > 1) {
                         for (int e = ta; e < nent; e += kApply) {
-                            const int2 rs = sm.L_rs[e];
-                            atomicAnd(sm.bm + (rs.x >> 5), ~(1u << (rs.x & 31)));
-                            atomicAnd(sm.bm + (rs.y >> 5), ~(1u << (rs.y & 31)));
+                            const int2 rs = sm.L_rs()[e];
+                            atomicAnd(sm.bm() + (rs.x >> 5), ~(1u << (rs.x & 31)));
+                            atomicAnd(sm.bm() + (rs.y >> 5), ~(1u << (rs.y & 31)));
                         }
                     }
                     total = nent;
                 } else {
                     // general path: exclusive scan of the segment counts, entries in phase order
-                    total = apply_scan(sm.s_off, nseg, ta, s_wsum);
+                    total = apply_scan(sm.s_off(), nseg, ta, s_wsum);
                     for (int e0 = 0; e0 < total; e0 += kPairCap) {
                         const int e1 = min(total, e0 + kPairCap);
                         for (int e = e0 + ta; e < e1; e += kApply) {
                             int lo = 0, hi = nseg;  // segment: s_off[lo] <= e < s_off[lo+1]
                             while (hi - lo > 1) {
                                 const int mid = (lo + hi) >> 1;
-                                if (sm.s_off[mid] <= e) lo = mid;
+                                if (sm.s_off()[mid] <= e) lo = mid;
                                 else hi = mid;
                             }
                             const int jb = lo / nsh;
-                            const int rank = e - sm.s_off[lo];
+                            const int rank = e - sm.s_off()[lo];
                             const size_t at =
                                 ((size_t)((k0 + jb) % a.rl) * nblk + (lo - jb * nsh)) * a.share + rank;
                             const int2 rs = __ldcg(lrsL + at);
                             const double2 dn = __ldcg(ldnL + at);
                             // segments with one entry had their Omega cells written above
-                            if (sm.s_off[lo + 1] - sm.s_off[lo] > 1) {
+                            if (sm.s_off()[lo + 1] - sm.s_off()[lo] > 1) {
                                 if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
                                 if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
                             }
-                            sm.L_rs[e - e0] = rs;
-                            sm.L_d[e - e0] = dn.x;
-                            sm.L_ph[e - e0] = jb;
+                            sm.L_rs()[e - e0] = rs;
+                            sm.L_d()[e - e0] = dn.x;
+                            sm.L_ph()[e - e0] = jb;
                             if (nb > 1) {
                                 const unsigned br = 1u << (rs.x & 31), bs = 1u << (rs.y & 31);
-                                const unsigned o1 = atomicOr(sm.bm + (rs.x >> 5), br);
-                                const unsigned o2 = atomicOr(sm.bm + (rs.y >> 5), bs);
+                                const unsigned o1 = atomicOr(sm.bm() + (rs.x >> 5), br);
+                                const unsigned o2 = atomicOr(sm.bm() + (rs.y >> 5), bs);
                                 if ((o1 & br) | (o2 & bs)) s_conflict = 1;
                             }
                         }
                         bar_apply();
                         const int conflict = s_conflict;
                         if (!conflict) {
-                            ROWS(sm.L_rs, sm.L_d, sm.L_ph, -1, 0, e1 - e0, w2, Wb, Tb, sm.ring, ta);
+                            ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, 0, e1 - e0, w2, Wb, Tb, sm.ring(), ta);
                         } else {
                             for (int jb = 0; jb < nb; ++jb) {
-                                const int lo = max(sm.s_off[jb * nsh], e0) - e0;
-                                const int hi = min(sm.s_off[(jb + 1) * nsh], e1) - e0;
-                                if (lo < hi) ROWS(sm.L_rs, sm.L_d, sm.L_ph, -1, lo, hi, w2, Wb, Tb, sm.ring, ta);
+                                const int lo = max(sm.s_off()[jb * nsh], e0) - e0;
+                                const int hi = min(sm.s_off()[(jb + 1) * nsh], e1) - e0;
+                                if (lo < hi) ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, lo, hi, w2, Wb, Tb, sm.ring(), ta);
                                 bar_apply();
                             }
                         }
                         bar_apply();
                         if (nb > 1) {
                             for (int e = ta; e < e1 - e0; e += kApply) {
-                                const int2 rs = sm.L_rs[e];
-                                atomicAnd(sm.bm + (rs.x >> 5), ~(1u << (rs.x & 31)));
-                                atomicAnd(sm.bm + (rs.y >> 5), ~(1u << (rs.y & 31)));
+                                const int2 rs = sm.L_rs()[e];
+                                atomicAnd(sm.bm() + (rs.x >> 5), ~(1u << (rs.x & 31)));
+                                atomicAnd(sm.bm() + (rs.y >> 5), ~(1u << (rs.y & 31)));
                             }
                         }
                         bar_apply();
@@ -1296,9 +1321,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 cph = ph0 + (k1 - k0);
                 cit = it0;
                 ++nbatch;
-                t_rows += clock64() - tr0;
+                t_rows += PCLK() - tr0;
             }
-            t_busy += clock64() - t0;
+            t_busy += PCLK() - t0;
             if (stopg >= 0 && C >= stopg) break;
         }
         if (prof && ta == 0) {
@@ -1319,6 +1344,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     }
 }
 
+#undef PCLK
 }  // namespace qb
 
 int qblock_cellcap(int share, int D) { return 2 * D * (share + 2 * (D - 1)) + 2 * share + 8; }
@@ -1344,11 +1370,12 @@ size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem) {
 
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
     const size_t smem = qblock_smem_bytes(args.p, nblk, args.share, args.D, args.tdiag_smem);
-    cudaError_t e = cudaFuncSetAttribute(qb::pcd_qblock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const void* fn = args.prof ? (const void*)qb::pcd_qblock_kernel<true> : (const void*)qb::pcd_qblock_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     QbArgs copy = args;
     void* kargs[] = {&copy};
-    return cudaLaunchCooperativeKernel((void*)qb::pcd_qblock_kernel, dim3(nblk), dim3(qb::kThreads), kargs, smem, st);
+    return cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(qb::kThreads), kargs, smem, st);
 }
 
 }  // namespace concord
