@@ -12,10 +12,12 @@ from bench import algorithmic_bytes  # noqa: E402
 
 csv_path, fits_path, out_path = sys.argv[1:4]
 rows = {}
+kernels = set()
 with open(csv_path) as f:
     lines = [ln for ln in f if not ln.startswith("==")]
 for r in csv.DictReader(lines):
     rows.setdefault(int(r["ID"]), {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    kernels.add(r["Kernel Name"].split("(")[0].replace("void ", ""))
 fits = json.load(open(fits_path))
 p = fits["p"]
 per = []
@@ -31,7 +33,7 @@ avg_traffic = sum(x["dram_bytes"] for x in per) / len(per)
 avg_alg = sum(x["algorithmic_bytes"] for x in per) / len(per)
 workload = f"ar2 p={p} n={fits['n']} lambda-path cold"
 out = {workload: {"dram_bytes_per_launch": avg_traffic, "algorithmic_bytes_per_launch": avg_alg,
-                  "kernel": "pcd_wform_kernel", "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+                  "kernel": ", ".join(sorted(kernels)), "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
                   "(one launch per lambda of the bench path, kernel replay)", "per_fit": per}}
 json.dump(out, open(out_path, "w"), indent=1)
 print(f"average per launch: dram {avg_traffic / 1e9:.2f} GB, algorithmic {avg_alg / 1e9:.2f} GB")
