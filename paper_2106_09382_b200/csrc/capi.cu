@@ -108,6 +108,7 @@ struct concord_solver {
     int lmax = 1, rd = 0, rl = 0, share = 0, nsh = 0;
     bool qb = false;       // temporally blocked chain (pcd_qblock.cu)
     int qb_D = 0, qb_NB = 0, qb_sr = 0, qb_rd = 0, qb_rl = 0;
+    int qb_nbuf = 1, qb_td = 0, qb_ring = 6;  // shared-memory plan of the blocked kernel
     double* qb_stW = nullptr;
     double* qb_stO = nullptr;
     double* qb_stT = nullptr;
@@ -288,11 +289,37 @@ int setup_qblock(concord_solver* s) {
     const int m = p + (p & 1) - 1;
     int D = QB_DEFAULT_D;
     if (const char* e = getenv("CONCORD_QB_D")) D = atoi(e);
-    if (D < 1) D = 1;
+    if (D < 2) D = 2;
     if (D > QB_DMAX) D = QB_DMAX;
     if (2 * D > m + 1) D = (m + 1) / 2;
-    const size_t smem = qblock_smem_bytes(p, s->nblk_tot, s->share, D, wform_tdiag_in_smem(p));
-    if (smem > 227 * 1024) return CONCORD_OK;  // stays on the per-phase kernel
+    // Shared-memory plan, first that fits 227 KB, in order of value: two cell buffers (the next
+    // block's cells built during the colours -- only useful when the colours leave chain warps
+    // free), the T diagonal in shared memory, the deepest cp.async row ring.
+    // overlap only while the prefetch group (chain warps the colours leave free) has at most
+    // ~5 cells per thread: beyond that part A outlasts the colours (measured at p=20000)
+    const int pf_threads = 32 * (WFORM_CHAIN_WARPS_QB - qblock_colour_warps(s->share, D));
+    bool can_overlap = pf_threads > 0 && qblock_cellcap(s->share, D) <= 5 * pf_threads;
+    if (const char* e = getenv("CONCORD_QB_NBUF")) can_overlap = can_overlap && atoi(e) >= 2;
+    struct Plan {
+        int nbuf, td, ring;
+    };
+    const Plan plans[] = {{2, 1, 6}, {2, 0, 6}, {1, 1, 6}, {1, 0, 6}, {1, 0, 4}, {1, 0, 2}};
+    const int td_ok = wform_tdiag_in_smem(p);
+    int chosen = -1;
+    for (int i = 0; i < (int)(sizeof(plans) / sizeof(plans[0])); ++i) {
+        const Plan& pl = plans[i];
+        if (pl.nbuf == 2 && !can_overlap) continue;
+        if (pl.td && !td_ok) continue;
+        const size_t smem = qblock_smem_bytes(p, s->nblk_tot, s->share, D, pl.td, pl.nbuf, pl.ring);
+        if (smem + 2048 <= 227 * 1024) {  // + static shared memory
+            chosen = i;
+            break;
+        }
+    }
+    if (chosen < 0) return CONCORD_OK;  // stays on the per-phase kernel
+    s->qb_nbuf = plans[chosen].nbuf;
+    s->qb_td = plans[chosen].td;
+    s->qb_ring = plans[chosen].ring;
     s->qb_D = D;
     s->qb_NB = (m + 1 + D - 1) / D;
     s->qb_sr = 4 * D + 4;
@@ -664,7 +691,9 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.T = a.T;
         q.Om = a.Om;
         q.tdiag = a.tdiag;
-        q.tdiag_smem = a.tdiag_smem;
+        q.tdiag_smem = s->qb_td;
+        q.nbuf = s->qb_nbuf;
+        q.ring_stages = s->qb_ring;
         q.diagv = s->qb_diagv;
         q.stW = s->qb_stW;
         q.stO = s->qb_stO;

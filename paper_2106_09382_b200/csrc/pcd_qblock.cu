@@ -50,7 +50,6 @@ constexpr int kBatch = WFORM_BATCH;
 constexpr int kUnroll = 2;
 constexpr int kRowUnroll = 2;
 constexpr int kDMax = QB_DMAX;
-constexpr int kAsyncStages = QB_ASYNC_STAGES;
 constexpr int kChainN = 32;   // batches with row conflicts up to this many entries: per-row chains
 
 __device__ __forceinline__ void bar_chain() { asm volatile("bar.sync 1, %0;" ::"n"(kChain) : "memory"); }
@@ -140,6 +139,12 @@ __device__ __forceinline__ int stage_mark(int b, int m, int D, int NB) {
     return (b < 3) ? -1 : block_at(b - 3, m, D, NB).g0 - 1;
 }
 
+// Chain warps the colours of a block need: one thread per pair of the widest colour.
+__host__ __device__ __forceinline__ int colour_warps(int share, int D) {
+    const int n = (share + 2 * (D - 1) + 31) / 32;
+    return n < kChainWarps ? n : kChainWarps;
+}
+
 // Exclusive scan of s[0..n) in place by the apply warps; returns the total (also in s[n]).
 __device__ int apply_scan(int* s, int n, int ta, int* s_wsum) {
     const int lane = ta & 31, wa = ta >> 5;
@@ -223,10 +228,9 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
 // 2 * kRowUnroll double2 pairs the registers allow. Each thread only reads the
 // slots it filled, so no barrier is needed; cp.async.wait_group orders them.
 // The item -> (entry, half, chunk) mapping and the FMA are those of apply_rows.
-#if QB_ASYNC_STAGES > 0
 __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double* L_d, const int* L_ph, int only,
                                                  int e_lo, int e_hi, int w2, double* __restrict__ Wb,
-                                                 const double* __restrict__ Tb, double2* ring, int ta) {
+                                                 const double* __restrict__ Tb, double2* ring, int ta, int S) {
     const int per = 2 * w2;
     const int items = (e_hi - e_lo) * per;
     const int nmine = items > ta ? (items - ta + kApply - 1) / kApply : 0;
@@ -241,11 +245,12 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
         off_w = (h ? rs.y : rs.x) * w2 + j2;
         off_t = (h ? rs.x : rs.y) * w2 + j2;
     };
+    int si = 0, sc = 0;  // ring slots of the next issue / the next completion
     auto issue = [&](int i) {
         int e, ow, ot;
         locate(i, e, ow, ot);
         if (only < 0 || L_ph[e] == only) {
-            double2* slot = ring + (size_t)((i % kAsyncStages) * 2) * kApply + ta;
+            double2* slot = ring + (size_t)(si * 2) * kApply + ta;
             const unsigned sw = (unsigned)__cvta_generic_to_shared(slot);
             const unsigned st = (unsigned)__cvta_generic_to_shared(slot + kApply);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sw),
@@ -256,22 +261,25 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
                          : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
+        si = (si + 1 == S) ? 0 : si + 1;
     };
-    // prologue: kAsyncStages - 1 items in flight; then one issue per completed item,
-    // and in the tail (nothing left to issue) wait for everything.
-    int ni = min(nmine, kAsyncStages - 1);
+    // prologue: S - 1 items in flight; then one issue per completed item, and in the
+    // tail (nothing left to issue) wait for everything.  S is 2, 4 or 6 (shared-memory budget).
+    int ni = min(nmine, S - 1);
     for (int i = 0; i < ni; ++i) issue(i);
     for (int j = 0; j < nmine; ++j) {
         if (ni < nmine) {
             issue(ni++);
-            asm volatile("cp.async.wait_group %0;" ::"n"(kAsyncStages - 1) : "memory");
+            if (S == 6) asm volatile("cp.async.wait_group 5;" ::: "memory");
+            else if (S == 4) asm volatile("cp.async.wait_group 3;" ::: "memory");
+            else asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         int e, ow, ot;
         locate(j, e, ow, ot);
         if (only < 0 || L_ph[e] == only) {
-            const double2* slot = ring + (size_t)((j % kAsyncStages) * 2) * kApply + ta;
+            const double2* slot = ring + (size_t)(sc * 2) * kApply + ta;
             double2 wv = slot[0];
             const double2 tv = slot[kApply];
             const double d = L_d[e];
@@ -279,9 +287,9 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
             wv.y = fma(d, tv.y, wv.y);
             reinterpret_cast<double2*>(Wb)[ow] = wv;
         }
+        sc = (sc + 1 == S) ? 0 : sc + 1;
     }
 }
-#endif
 
 
 // Rows of a batch whose phases move some row more than once (entries [0, nent), all in
@@ -355,12 +363,8 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
     }
 }
 
-#if QB_ASYNC_STAGES > 0
 #define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) \
-    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_)
-#else
-#define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) apply_rows(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ta_)
-#endif
+    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_, a.ring_stages)
 
 __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target, int blk,
                                              long long* hang) {
@@ -398,13 +402,13 @@ struct Smem {
     unsigned o_cC;  // [cellcap] column of each block cell
     unsigned o_cW;  // [cellcap] cell value brought forward to the start of the block
     unsigned o_cO;  // [cellcap] Omega of the cell
-    unsigned o_cT;  // [cellcap][kDMax-1] T entries of the block's earlier phases
+    unsigned o_cT;  // [nbuf][cellcap][D-1] T entries of the block's earlier phases
     unsigned o_sd;  // [kDMax][rmax] delta of each pair of the block's phases (extended ranges)
-    unsigned o_cQ;  // [cellcap][kDMax-1] index into sd[i] of the cell row's pair at in-block phase i
+    unsigned o_cQ;  // [nbuf][cellcap][D-1] index into sd[i] of the cell row's pair at in-block phase i
     unsigned o_snv;  // [kDMax][share] new value of each own pair of the block's colours
     unsigned o_hd_rs;  // [kBatch * nblk] first entry of each list segment of a batch
     unsigned o_hd_dn;  // [kBatch * nblk]
-    unsigned o_ring;  // [kAsyncStages][2][kApply] per-thread cp.async slots of the row streams
+    unsigned o_ring;  // [ring_stages][2][kApply] per-thread cp.async slots of the row streams
     __device__ __forceinline__ int2* L_rs() const { return reinterpret_cast<int2*>(qb_smem + o_L_rs); }
     __device__ __forceinline__ double* L_d() const { return reinterpret_cast<double*>(qb_smem + o_L_d); }
     __device__ __forceinline__ double* L_new() const { return reinterpret_cast<double*>(qb_smem + o_L_new); }
@@ -443,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     const int b = blockIdx.x, bl = b, nblk = gridDim.x;
     const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half;
     const int D = a.D, NB = a.NB;
+    const int dm1 = D - 1;  // stride of the per-cell arrays cT, cQ
     const int c0 = b * w;
     const int wl = max(0, min(w, p - c0));
     const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
@@ -467,17 +472,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         sm.o_L_ph = take(sizeof(int) * kPairCap);
         sm.o_s_off = take(sizeof(int) * ((size_t)kBatch * nblk + 1));
         sm.o_bm = take(sizeof(unsigned) * (size_t)((p + 31) / 32));
-        sm.o_cX = take(sizeof(int) * 2 * (size_t)a.cellcap);
-        sm.o_cC = take(sizeof(int) * 2 * (size_t)a.cellcap);
-        sm.o_cW = take(sizeof(double) * 2 * (size_t)a.cellcap);
-        sm.o_cO = take(sizeof(double) * 2 * (size_t)a.cellcap);
-        sm.o_cT = take(sizeof(double) * 2 * (size_t)a.cellcap * (kDMax - 1));
+        sm.o_cX = take(sizeof(int) * a.nbuf * (size_t)a.cellcap);
+        sm.o_cC = take(sizeof(int) * a.nbuf * (size_t)a.cellcap);
+        sm.o_cW = take(sizeof(double) * a.nbuf * (size_t)a.cellcap);
+        sm.o_cO = take(sizeof(double) * a.nbuf * (size_t)a.cellcap);
+        sm.o_cT = take(sizeof(double) * a.nbuf * (size_t)a.cellcap * dm1);
         sm.o_sd = take(sizeof(double) * (size_t)kDMax * a.rmax);
-        sm.o_cQ = take(sizeof(short) * 2 * (size_t)a.cellcap * (kDMax - 1));
+        sm.o_cQ = take(sizeof(short) * a.nbuf * (size_t)a.cellcap * dm1);
         sm.o_snv = take(sizeof(double) * (size_t)kDMax * a.share);
         sm.o_hd_rs = take(sizeof(int2) * (size_t)kBatch * nblk);
         sm.o_hd_dn = take(sizeof(double2) * (size_t)kBatch * nblk);
-        sm.o_ring = kAsyncStages ? take(sizeof(double2) * 2 * (size_t)kApply * kAsyncStages) : 0xffffffffu;
+        sm.o_ring = take(sizeof(double2) * 2 * (size_t)kApply * a.ring_stages);
         sm.o_td = a.tdiag_smem ? take(sizeof(double) * (size_t)p) : 0xffffffffu;
     }
     if (a.tdiag_smem)
@@ -523,8 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         // prefetch group) meanwhile build part A of the next block's cells, so only part B
         // (the previous block's deltas) is left between a barrier and the colours.  When the
         // colours need every chain warp, part A runs after the arrive instead.
-        const int ncw = min(kChainWarps, (a.share + 2 * (D - 1) + 31) / 32);
-        const bool overlap = ncw < kChainWarps;
+        const bool overlap = colour_warps(a.share, D) < kChainWarps && a.nbuf == 2;
+        const int ncw = overlap ? colour_warps(a.share, D) : kChainWarps;
         const int cg0 = kChain - 32 * ncw;  // first thread of the colour group
         const int ng = 32 * ncw;
         const bool in_cg = tc >= cg0;
@@ -554,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const int hiA = (B >= 1) ? block_at(B - 1, m, D, NB).g0 : 0;
             const int na = hiA - (CpB + 1);
             Layout& L = s_ly[B & 1];
-            const int cb = (B & 1) * a.cellcap;
+            const int cb = (a.nbuf == 2) ? (B & 1) * a.cellcap : 0;
             // layout: colour d = 0..nbc-1 covers pairs [lo_d, hi_d), two cells per pair;
             // then the diagonal cells (rows of the own pairs at colour m-1)
             if (tc == 0) {
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     int pos = (x == 0) ? 0 : 1 + (x - 1 + kB.ph0) % m;
                     for (int i = 0; i < d; ++i) {
                         const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
-                        sm.cQ()[(size_t)(cb + ci) * (kDMax - 1) + i] = (short)(qi - L.lo[i]);
+                        sm.cQ()[(size_t)(cb + ci) * dm1 + i] = (short)(qi - L.lo[i]);
                         if (x != 0) pos = (pos == m) ? 1 : pos + 1;
                     }
                 }
@@ -658,7 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 sm.cW()[cb + ci] = val;
                 sm.cO()[cb + ci] = om;
 #pragma unroll
-                for (int i = 0; i < kDMax - 1; ++i) sm.cT()[(size_t)(cb + ci) * (kDMax - 1) + i] = tin[i];
+                for (int i = 0; i < kDMax - 1; ++i)
+                    if (i < dm1) sm.cT()[(size_t)(cb + ci) * dm1 + i] = tin[i];
             }
         };
         int blk = 0;
@@ -697,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const bool has_diag = (k.ph0 + k.len - 1 == m);
             const int nbc = k.len - (has_diag ? 1 : 0);  // colour phases of the block
             const Layout& L = s_ly[blk & 1];
-            const int cb = (blk & 1) * a.cellcap;
+            const int cb = (a.nbuf == 2) ? (blk & 1) * a.cellcap : 0;
             if (blk == 0) {
                 cells_a(0, kChain, 1);
                 bar_chain();
@@ -707,36 +713,52 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const int hiA = (blk >= 1) ? block_at(blk - 1, m, D, NB).g0 : 0;
                 const int nbv = k.g0 - hiA;
                 const int ntotB = L.ncell + (has_diag ? 2 * (q_hi - q_lo) : 0);
-                for (int ci = tc; ci < ntotB; ci += kChain) {
-                    const int x = sm.cX()[cb + ci];
-                    if (x < 0) continue;
-                    double dj[kDMax];
-                    int slot = L.rdb;
+                // two cells per step: both cells' ring loads, then both cells' T loads, back to back
+                for (int c0i = tc; c0i < ntotB; c0i += 2 * kChain) {
+                    double dj[2][kDMax];
+                    int xs[2];
 #pragma unroll
-                    for (int u = 0; u < kDMax; ++u) {
-                        dj[u] = ldcg_if(a.dring + (size_t)slot * p + x, u < nbv);
-                        slot = (slot + 1 == a.rd) ? 0 : slot + 1;
-                    }
-                    unsigned mask = 0u;
-#pragma unroll
-                    for (int u = 0; u < kDMax; ++u)
-                        if (dj[u] != 0.0) mask |= 1u << u;
-                    if (mask) {
-                        const int c = sm.cC()[cb + ci];
-                        const int cs = c / w;  // slab of column c
-                        const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
-                        double tj[kDMax];
-                        PartnerWalk pw(x, L.phb, m);
+                    for (int h = 0; h < 2; ++h) {
+                        const int ci = c0i + h * kChain;
+                        xs[h] = (ci < ntotB) ? sm.cX()[cb + ci] : -1;
+                        int slot = L.rdb;
 #pragma unroll
                         for (int u = 0; u < kDMax; ++u) {
-                            tj[u] = ldcg_if(Tc + (long long)pw.y() * w, (mask >> u) & 1u);
-                            pw.next();
+                            dj[h][u] = ldcg_if(a.dring + (size_t)slot * p + max(xs[h], 0), xs[h] >= 0 && u < nbv);
+                            slot = (slot + 1 == a.rd) ? 0 : slot + 1;
                         }
-                        double val = sm.cW()[cb + ci];
+                    }
+                    unsigned mask[2] = {0u, 0u};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
 #pragma unroll
                         for (int u = 0; u < kDMax; ++u)
-                            if (mask & (1u << u)) val = fma(dj[u], tj[u], val);
-                        sm.cW()[cb + ci] = val;
+                            if (dj[h][u] != 0.0) mask[h] |= 1u << u;
+                    if (mask[0] | mask[1]) {
+                        double tj[2][kDMax];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int ci = c0i + h * kChain;
+                            const int c = mask[h] ? sm.cC()[cb + ci] : 0;
+                            const int cs = c / w;  // slab of column c
+                            const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
+                            PartnerWalk pw(max(xs[h], 0), L.phb, m);
+#pragma unroll
+                            for (int u = 0; u < kDMax; ++u) {
+                                tj[h][u] = ldcg_if(Tc + (long long)pw.y() * w, (mask[h] >> u) & 1u);
+                                pw.next();
+                            }
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (!mask[h]) continue;
+                            const int ci = c0i + h * kChain;
+                            double val = sm.cW()[cb + ci];
+#pragma unroll
+                            for (int u = 0; u < kDMax; ++u)
+                                if (mask[h] & (1u << u)) val = fma(dj[h][u], tj[h][u], val);
+                            sm.cW()[cb + ci] = val;
+                        }
                     }
                 }
             }
@@ -778,14 +800,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 v2[side] = sm.cW()[ci + side];
 #pragma unroll
                                 for (int i = 0; i < kDMax - 1; ++i)
-                                    qi[side][i] = (i < d) ? sm.cQ()[(size_t)(ci + side) * (kDMax - 1) + i] : (short)0;
+                                    qi[side][i] = (i < d) ? sm.cQ()[(size_t)(ci + side) * dm1 + i] : (short)0;
                             }
 #pragma unroll
                             for (int side = 0; side < 2; ++side)
 #pragma unroll
                                 for (int i = 0; i < kDMax - 1; ++i) {
                                     di[side][i] = (i < d) ? sm.sd()[(size_t)i * a.rmax + qi[side][i]] : 0.0;
-                                    ti[side][i] = (i < d) ? sm.cT()[(size_t)(ci + side) * (kDMax - 1) + i] : 0.0;
+                                    ti[side][i] = (i < d) ? sm.cT()[(size_t)(ci + side) * dm1 + i] : 0.0;
                                 }
 #pragma unroll
                             for (int side = 0; side < 2; ++side)
@@ -872,8 +894,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         if (x < 0) continue;
                         double val = sm.cW()[cc];
                         for (int i = 0; i < nbc; ++i) {
-                            const double di = sm.sd()[(size_t)i * a.rmax + sm.cQ()[(size_t)cc * (kDMax - 1) + i]];
-                            if (di != 0.0) val = fma(di, sm.cT()[(size_t)cc * (kDMax - 1) + i], val);
+                            const double di = sm.sd()[(size_t)i * a.rmax + sm.cQ()[(size_t)cc * dm1 + i]];
+                            if (di != 0.0) val = fma(di, sm.cT()[(size_t)cc * dm1 + i], val);
                         }
                         const double om = sm.cO()[cc];
                         const double nv = diag_from_dot(val, om, TD(x), a.n);
@@ -1351,25 +1373,28 @@ int qblock_cellcap(int share, int D) { return 2 * D * (share + 2 * (D - 1)) + 2 
 
 int qblock_rmax(int share, int D) { return share + 2 * (D - 1) + 2; }
 
-size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem) {
+size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages) {
     auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
-    const size_t cap = 2 * (size_t)qblock_cellcap(share, D);  // two cell buffers
+    const size_t cap = (size_t)nbuf * qblock_cellcap(share, D);  // cell buffers
     size_t b = 0;
     b += al(sizeof(int2) * qb::kPairCap) + 2 * al(sizeof(double) * qb::kPairCap) + al(sizeof(int) * qb::kPairCap);
     b += al(sizeof(int) * ((size_t)qb::kBatch * nblk + 1));
     b += al(sizeof(unsigned) * (size_t)((p + 31) / 32));
-    b += 2 * al(sizeof(int) * cap) + 2 * al(sizeof(double) * cap) + al(sizeof(double) * cap * (qb::kDMax - 1));
+    b += 2 * al(sizeof(int) * cap) + 2 * al(sizeof(double) * cap) + al(sizeof(double) * cap * (D - 1));
     b += al(sizeof(double) * (size_t)qb::kDMax * qblock_rmax(share, D));
-    b += al(sizeof(short) * cap * (qb::kDMax - 1));
-    b += al(sizeof(double2) * 2 * (size_t)qb::kApply * qb::kAsyncStages);
+    b += al(sizeof(short) * cap * (D - 1));
     b += al(sizeof(double) * (size_t)qb::kDMax * share);
     b += al(sizeof(int2) * (size_t)qb::kBatch * nblk) + al(sizeof(double2) * (size_t)qb::kBatch * nblk);
+    b += al(sizeof(double2) * 2 * (size_t)qb::kApply * ring_stages);
     if (tdiag_smem) b += al(sizeof(double) * (size_t)p);
     return b;
 }
 
+// Warps of the colour group for a CTA share (the chain warps the colours need).
+int qblock_colour_warps(int share, int D) { return qb::colour_warps(share, D); }
+
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
-    const size_t smem = qblock_smem_bytes(args.p, nblk, args.share, args.D, args.tdiag_smem);
+    const size_t smem = qblock_smem_bytes(args.p, nblk, args.share, args.D, args.tdiag_smem, args.nbuf, args.ring_stages);
     const void* fn = args.prof ? (const void*)qb::pcd_qblock_kernel<true> : (const void*)qb::pcd_qblock_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

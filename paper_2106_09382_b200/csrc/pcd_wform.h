@@ -84,7 +84,7 @@ struct WformArgs {
 
 // Temporally blocked variant (pcd_qblock.cu): D colour phases per grid barrier.
 #ifndef QB_DMAX
-#define QB_DMAX 8
+#define QB_DMAX 4
 #endif
 #ifndef QB_DEFAULT
 #define QB_DEFAULT 1        // 1: single-device solvers use the temporally blocked kernel by default
@@ -92,12 +92,10 @@ struct WformArgs {
 #ifndef QB_CHAIN_WARPS
 #define QB_CHAIN_WARPS 6     // chain warps of the blocked kernel (the block's cells are loaded in parallel)
 #endif
-#ifndef QB_ASYNC_STAGES
-#define QB_ASYNC_STAGES 6    // per-thread cp.async ring depth of the blocked kernel's row streams (0: registers)
-#endif
 #ifndef QB_ASYNC_HEADS
 #define QB_ASYNC_HEADS 1     // blocked kernel: segment heads copied asynchronously while the apply warps stage
 #endif
+#define WFORM_CHAIN_WARPS_QB QB_CHAIN_WARPS
 #ifndef QB_DEFAULT_D
 #define QB_DEFAULT_D 4
 #endif
@@ -137,10 +135,13 @@ struct QbArgs {
     int* status;
     unsigned long long* prof;
     long long* hang;       // [8] mapped host memory: watchdog report (what+1, CTA, block, 4 values)
+    int nbuf;              // cell buffers: 2 = next block's cells built during the colours
+    int ring_stages;       // cp.async row-ring depth (2, 4 or 6)
 };
 int qblock_cellcap(int share, int D);
 int qblock_rmax(int share, int D);
-size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem);
+size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
+int qblock_colour_warps(int share, int D);
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st);
 
 // Lag cap for a slab width (bounded by the stage ring's shared memory) and m.
