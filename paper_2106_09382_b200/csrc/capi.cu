@@ -693,6 +693,8 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.tdiag = a.tdiag;
         q.tdiag_smem = s->qb_td;
         q.nbuf = s->qb_nbuf;
+        q.colour_warps_min = 1;
+        if (const char* e = getenv("CONCORD_QB_CW")) q.colour_warps_min = atoi(e);
         q.ring_stages = s->qb_ring;
         q.diagv = s->qb_diagv;
         q.stW = s->qb_stW;

@@ -528,8 +528,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         // prefetch group) meanwhile build part A of the next block's cells, so only part B
         // (the previous block's deltas) is left between a barrier and the colours.  When the
         // colours need every chain warp, part A runs after the arrive instead.
-        const bool overlap = colour_warps(a.share, D) < kChainWarps && a.nbuf == 2;
-        const int ncw = overlap ? colour_warps(a.share, D) : kChainWarps;
+        const int ncw0 = max(colour_warps(a.share, D), min(a.colour_warps_min, kChainWarps));
+        const bool overlap = ncw0 < kChainWarps && a.nbuf == 2;
+        const int ncw = overlap ? ncw0 : kChainWarps;
         const int cg0 = kChain - 32 * ncw;  // first thread of the colour group
         const int ng = 32 * ncw;
         const bool in_cg = tc >= cg0;

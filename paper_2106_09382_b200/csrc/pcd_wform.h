@@ -137,6 +137,7 @@ struct QbArgs {
     long long* hang;       // [8] mapped host memory: watchdog report (what+1, CTA, block, 4 values)
     int nbuf;              // cell buffers: 2 = next block's cells built during the colours
     int ring_stages;       // cp.async row-ring depth (2, 4 or 6)
+    int colour_warps_min;  // lower bound on the colour group's warps (tuning)
 };
 int qblock_cellcap(int share, int D);
 int qblock_rmax(int share, int D);

@@ -48,6 +48,8 @@ def test_p5000_tight_fit_properties(gram5000):
 def test_p20000_shards_bitwise():
     x = synth.center(synth.sample_mvn_ar2_banded(20000, 5000, seed=0))
     with cb.Solver(20000) as s1:
+        # the blocked kernel (single cell buffer plan at this share), not the per-phase fallback
+        assert s1.layout()["kernel"] == 4
         s1.gram_from_data(cb.DataMatrix(x, centered=True))
         g = s1.gram()
         r1 = s1.fit(0.3, 1e-5, 2, raise_on_cap=False)
@@ -90,3 +92,9 @@ def test_device_ar2_sampler_moments():
         s1.gram_from_ar2(n, seed=3)
         g = s1.gram()
     np.testing.assert_allclose(g.t, synth.host_gram(x), rtol=1e-12, atol=1e-9)
+
+
+def test_largest_config_runs_the_blocked_kernel():
+    """configs[4] (p=50000) must fit the blocked kernel's shared-memory plan."""
+    with cb.Solver(50000) as s:
+        assert s.layout()["kernel"] == 4
