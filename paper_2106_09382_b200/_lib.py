@@ -196,6 +196,55 @@ class _PinnedOwner:
             pass
 
 
+class _PooledOwner:
+    """A pooled page-locked block: returned to the pool (not freed) when the last view dies."""
+
+    def __init__(self, addr, nbytes):
+        self.addr = addr
+        self.nbytes = nbytes
+
+    def __del__(self):
+        try:
+            free = _POOL.setdefault(self.nbytes, [])
+            if len(free) < _POOL_KEEP:
+                free.append(self.addr)
+            else:
+                load().concord_host_free(ctypes.c_void_p(self.addr))
+        except Exception:
+            pass
+
+
+_POOL = {}  # nbytes -> free page-locked blocks
+_POOL_KEEP = 4
+
+
+def pooled_pinned_empty(shape, dtype=None):
+    """numpy array in page-locked host memory, recycled through a pool.
+
+    The result arrays of consecutive fits (200 MB at p=5000) then land in memory
+    that is already pinned and faulted in: a device->host copy runs at DMA speed
+    instead of paying page faults on fresh pageable memory (~45 ms per fit at
+    p=5000).  The array owns its block until it is garbage collected.
+    """
+    import numpy as np
+
+    dtype = np.dtype(dtype or np.float64)
+    count = int(np.prod(shape))
+    nbytes = max(count * dtype.itemsize, 1)
+    if device_count() < 1:
+        return np.empty(shape, dtype)
+    free = _POOL.get(nbytes)
+    if free:
+        addr = free.pop()
+    else:
+        raw = ctypes.c_void_p()
+        check(load().concord_host_alloc(nbytes, ctypes.byref(raw)))
+        addr = raw.value
+    buf = (ctypes.c_char * nbytes).from_address(addr)
+    buf._owner = _PooledOwner(addr, nbytes)
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+
 def pinned_empty(shape, dtype=None):
     """numpy array in page-locked host memory (cudaHostAlloc); plain memory if no device."""
     import numpy as np

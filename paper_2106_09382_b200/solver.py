@@ -255,7 +255,7 @@ class Solver:
 
     def omega(self, out=None):
         if out is None:
-            out = np.empty((self.p, self.p))
+            out = _lib.pooled_pinned_empty((self.p, self.p))
         _lib.check(_lib.load().concord_solver_get_omega(self._h, _lib.ptr(out), _lib.HOST))
         return out
 

@@ -337,3 +337,22 @@ def test_blocked_kernel_bitwise_equals_per_phase_kernel(p, lam, monkeypatch):
         assert np.array_equal(om, om0), d
         assert np.array_equal(dl, dl0), d
         np.testing.assert_allclose(ob, ob0, rtol=1e-12)
+
+
+def test_result_arrays_are_independent_pinned_pool(golden):
+    """Omega results come from a pool of page-locked blocks: a live report's array is never
+    reused, and a freed one is recycled without disturbing the others."""
+    c = case(golden, "ar2_p100_n50_l0.1")
+    with cb.Solver(c["p"]) as s:
+        s.set_gram(cb.GramMatrix(c["t"], c["n"]))
+        r1 = s.fit(0.3, 1e-5, 5000)
+        keep = r1.estimate.omega.copy()
+        r2 = s.fit(0.1, 1e-5, 5000)
+        assert not np.shares_memory(r1.estimate.omega, r2.estimate.omega)
+        assert np.array_equal(r1.estimate.omega, keep)
+        del r2
+        r3 = s.fit(0.2, 1e-5, 5000)
+        assert not np.shares_memory(r1.estimate.omega, r3.estimate.omega)
+        assert np.array_equal(r1.estimate.omega, keep)
+        r4 = s.fit(0.1, 1e-5, 5000)
+        assert_close_support(r4.estimate.omega, c["omega"])
