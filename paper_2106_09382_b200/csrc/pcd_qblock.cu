@@ -973,6 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         int staged = 1;  // highest block staged
         long long t_busy = 0, t_idle = 0, nbatch = 0, t_diag = 0, t_stage = 0, t_heads = 0, t_rows = 0;
         unsigned long long idle_since = 0;  // watchdog (thread ta == 0)
+        int last_total = 0;                 // entries of the previous colour batch
         while (true) {
             const long long t0 = PCLK();
             bar_apply();
@@ -1006,6 +1007,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const int sb = staged + 1;
             const int Cp = stage_mark(sb, m, D, NB);
             const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 3 && Cp <= E - 1 && C >= Cp - a.stage_window;
+            // and the block after it in the same pass when it is eligible too and the batches are
+            // small (the apply then gets a block ahead of the chain's needs and its latency-bound
+            // batches grow to two blocks; dense batches are bandwidth-bound and gain nothing)
+            const int Cp2 = stage_mark(sb + 1, m, D, NB);
+            const bool can2 = can_stage && last_total <= 256 && sb + 1 <= cblk + 3 && Cp2 <= E - 1 &&
+                              C >= Cp2 - a.stage_window;
             if (!have && !can_stage) {
                 t_idle += PCLK() - t0;
                 // the chain stopped after this slab already reached the last phase: done
@@ -1067,8 +1074,15 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             // ---- stage block sb: cells brought forward from this slab's watermark C to C'
             if (can_stage) {
                 const long long ts = PCLK();
-                const Blk kb = block_at(sb, m, D, NB);
-                for (int idx = ta; idx < kb.len * wl; idx += kApply) {
+                const Blk kb0 = block_at(sb, m, D, NB);
+                const Blk kb1 = block_at(sb + 1, m, D, NB);
+                const int n0 = kb0.len * wl;
+                const int nst = n0 + (can2 ? kb1.len * wl : 0);
+                for (int idx2 = ta; idx2 < nst; idx2 += kApply) {
+                    const bool second = idx2 >= n0;
+                    const Blk kb = second ? kb1 : kb0;
+                    const int Cp = second ? Cp2 : stage_mark(sb, m, D, NB);
+                    const int idx = second ? idx2 - n0 : idx2;
                     const int i = idx / wl, j = idx - i * wl;
                     const int Q = kb.g0 + i;
                     const int c = c0 + j;
@@ -1149,7 +1163,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             bar_apply();
             const long long th1 = PCLK();
             if (can_stage) {
-                staged = sb;
+                staged = can2 ? sb + 1 : sb;
                 if (ta == 0) {
                     __threadfence_block();
                     st_vol(&s_staged, staged);
@@ -1344,6 +1358,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 cph = ph0 + (k1 - k0);
                 cit = it0;
                 ++nbatch;
+                last_total = total;
                 t_rows += PCLK() - tr0;
             }
             t_busy += PCLK() - t0;
