@@ -152,6 +152,23 @@ int concord_ar2_data_f64(int64_t p, int64_t n, uint64_t seed, double* X_out, int
 int concord_solver_gram_from_ar2(concord_solver* s, int64_t n, uint64_t seed);
 
 /* ---- pinned host buffers for fast H2D/D2H of T and Omega ---------------- */
+/* Kernel plan the library chooses for a p x p problem on one device with n_sms SMs (one CTA per
+ * SM, default slab layout): the temporally blocked fit kernel with colours_per_barrier colours
+ * per grid barrier and the given shared-memory plan, or colours_per_barrier = 0 for the
+ * per-phase kernel.  Host-only (no device needed).  Replaces no reference interface: the
+ * reference runs one host loop for every p (solver.py:254-294). */
+typedef struct {
+    int32_t colours_per_barrier; /* D; 0 = per-phase kernel */
+    int32_t cell_buffers;        /* 2 = next block's cells built during the colours */
+    int32_t tdiag_in_smem;
+    int32_t ring_stages;         /* cp.async row-ring depth */
+    int64_t smem_bytes;          /* dynamic shared memory per CTA */
+    int32_t slab_width;
+    int32_t ctas;
+    int32_t share;               /* circle-schedule pairs per CTA */
+} concord_blocked_plan_t;
+int concord_blocked_plan(int64_t p, int32_t n_sms, concord_blocked_plan_t* out);
+
 int concord_host_alloc(int64_t bytes, void** out);
 int concord_host_free(void* ptr);
 

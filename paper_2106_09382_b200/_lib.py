@@ -32,7 +32,7 @@ EXPORTS = (
     "concord_solver_create_sharded", "concord_solver_layout", "concord_shard_create",
     "concord_shard_ipc_handle", "concord_shard_open_peers", "concord_solver_objective_parts",
     "concord_solver_check_optimality", "concord_solver_estimate_entries",
-    "concord_ar2_data_f64", "concord_solver_gram_from_ar2",
+    "concord_ar2_data_f64", "concord_solver_gram_from_ar2", "concord_blocked_plan",
 )
 
 ABI_VERSION = 2
@@ -76,6 +76,20 @@ class Layout(ctypes.Structure):
         ("ncols", ctypes.c_int64),
         ("lag_cap", ctypes.c_int32),
         ("kernel", ctypes.c_int32),
+    ]
+
+
+class BlockedPlan(ctypes.Structure):
+    """concord_blocked_plan_t: the fit-kernel plan for a problem size (host-only query)."""
+    _fields_ = [
+        ("colours_per_barrier", ctypes.c_int32),
+        ("cell_buffers", ctypes.c_int32),
+        ("tdiag_in_smem", ctypes.c_int32),
+        ("ring_stages", ctypes.c_int32),
+        ("smem_bytes", ctypes.c_int64),
+        ("slab_width", ctypes.c_int32),
+        ("ctas", ctypes.c_int32),
+        ("share", ctypes.c_int32),
     ]
 
 
@@ -123,6 +137,7 @@ def load(build_if_missing=True):
             "concord_solver_edge_count": ([vp, ctypes.POINTER(i64)], ctypes.c_int),
             "concord_solver_sweep_stats": ([vp, vp, i32, ctypes.POINTER(i32)], ctypes.c_int),
             "concord_host_alloc": ([i64, ctypes.POINTER(vp)], ctypes.c_int),
+            "concord_blocked_plan": ([i64, i32, ctypes.POINTER(BlockedPlan)], ctypes.c_int),
             "concord_host_free": ([vp], ctypes.c_int),
             "concord_gram_f64": ([vp, i64, i64, vp, i32], ctypes.c_int),
             "concord_pcd_fit": ([vp, i64, d, ctypes.POINTER(FitParams), vp, ctypes.POINTER(FitResult), vp, vp,
@@ -216,6 +231,13 @@ class _PooledOwner:
 
 _POOL = {}  # nbytes -> free page-locked blocks
 _POOL_KEEP = 4
+
+
+def blocked_plan(p, n_sms=148):
+    """Fit-kernel plan for a p x p problem on one device with n_sms SMs (no device needed)."""
+    out = BlockedPlan()
+    check(load().concord_blocked_plan(int(p), int(n_sms), ctypes.byref(out)))
+    return {f: getattr(out, f) for f, _ in BlockedPlan._fields_}
 
 
 def pooled_pinned_empty(shape, dtype=None):

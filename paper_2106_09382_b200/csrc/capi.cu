@@ -283,43 +283,51 @@ WformCopies copies(const concord_solver* s) {
     return x;
 }
 
+// Shared-memory plan of the blocked kernel for p (slabs of a default single-device layout:
+// nblk CTAs, `share` pairs each), first that fits 227 KB, in order of value: two cell buffers
+// (the next block's cells built during the colours -- only useful while the prefetch group, the
+// chain warps the colours leave free, has at most ~5 cells per thread; beyond that part A
+// outlasts the colours, measured at p=20000), the T diagonal in shared memory, the deepest
+// cp.async row ring.  Returns false when nothing fits (the per-phase kernel then runs).
+struct QbPlan {
+    int D, nbuf, td, ring;
+    size_t smem;
+};
+static bool qblock_plan(int p, int nblk, int share, int D, bool allow_overlap, QbPlan* out) {
+    const int m = p + (p & 1) - 1;
+    if (D < 2) D = 2;
+    if (D > QB_DMAX) D = QB_DMAX;
+    if (2 * D > m + 1) D = (m + 1) / 2;
+    const int pf_threads = 32 * (WFORM_CHAIN_WARPS_QB - qblock_colour_warps(share, D));
+    const bool can_overlap = allow_overlap && pf_threads > 0 && qblock_cellcap(share, D) <= 5 * pf_threads;
+    static const int plans[][3] = {{2, 1, 6}, {2, 0, 6}, {1, 1, 6}, {1, 0, 6}, {1, 0, 4}, {1, 0, 2}};
+    const int td_ok = wform_tdiag_in_smem(p);
+    for (const auto& pl : plans) {
+        if (pl[0] == 2 && !can_overlap) continue;
+        if (pl[1] && !td_ok) continue;
+        const size_t smem = qblock_smem_bytes(p, nblk, share, D, pl[1], pl[0], pl[2]);
+        if (smem + 2048 <= 227 * 1024) {  // + static shared memory
+            *out = QbPlan{D, pl[0], pl[1], pl[2], smem};
+            return true;
+        }
+    }
+    return false;
+}
+
 // Buffers of the temporally blocked chain (pcd_qblock.cu); leaves s->qb false when it does not fit.
 int setup_qblock(concord_solver* s) {
     const int p = s->p;
     const int m = p + (p & 1) - 1;
     int D = QB_DEFAULT_D;
     if (const char* e = getenv("CONCORD_QB_D")) D = atoi(e);
-    if (D < 2) D = 2;
-    if (D > QB_DMAX) D = QB_DMAX;
-    if (2 * D > m + 1) D = (m + 1) / 2;
-    // Shared-memory plan, first that fits 227 KB, in order of value: two cell buffers (the next
-    // block's cells built during the colours -- only useful when the colours leave chain warps
-    // free), the T diagonal in shared memory, the deepest cp.async row ring.
-    // overlap only while the prefetch group (chain warps the colours leave free) has at most
-    // ~5 cells per thread: beyond that part A outlasts the colours (measured at p=20000)
-    const int pf_threads = 32 * (WFORM_CHAIN_WARPS_QB - qblock_colour_warps(s->share, D));
-    bool can_overlap = pf_threads > 0 && qblock_cellcap(s->share, D) <= 5 * pf_threads;
-    if (const char* e = getenv("CONCORD_QB_NBUF")) can_overlap = can_overlap && atoi(e) >= 2;
-    struct Plan {
-        int nbuf, td, ring;
-    };
-    const Plan plans[] = {{2, 1, 6}, {2, 0, 6}, {1, 1, 6}, {1, 0, 6}, {1, 0, 4}, {1, 0, 2}};
-    const int td_ok = wform_tdiag_in_smem(p);
-    int chosen = -1;
-    for (int i = 0; i < (int)(sizeof(plans) / sizeof(plans[0])); ++i) {
-        const Plan& pl = plans[i];
-        if (pl.nbuf == 2 && !can_overlap) continue;
-        if (pl.td && !td_ok) continue;
-        const size_t smem = qblock_smem_bytes(p, s->nblk_tot, s->share, D, pl.td, pl.nbuf, pl.ring);
-        if (smem + 2048 <= 227 * 1024) {  // + static shared memory
-            chosen = i;
-            break;
-        }
-    }
-    if (chosen < 0) return CONCORD_OK;  // stays on the per-phase kernel
-    s->qb_nbuf = plans[chosen].nbuf;
-    s->qb_td = plans[chosen].td;
-    s->qb_ring = plans[chosen].ring;
+    bool allow_overlap = true;
+    if (const char* e = getenv("CONCORD_QB_NBUF")) allow_overlap = atoi(e) >= 2;
+    QbPlan plan;
+    if (!qblock_plan(p, s->nblk_tot, s->share, D, allow_overlap, &plan)) return CONCORD_OK;  // per-phase kernel
+    D = plan.D;
+    s->qb_nbuf = plan.nbuf;
+    s->qb_td = plan.td;
+    s->qb_ring = plan.ring;
     s->qb_D = D;
     s->qb_NB = (m + 1 + D - 1) / D;
     s->qb_sr = 4 * D + 4;
@@ -1035,6 +1043,32 @@ int concord_solver_gram_from_ar2(concord_solver* s, int64_t n, uint64_t seed) {
     if (!rc) rc = concord_solver_gram_from_data(s, X, n, CONCORD_DEVICE);
     cudaFree(X);
     return rc;
+}
+
+int concord_blocked_plan(int64_t p, int32_t n_sms, concord_blocked_plan_t* out) {
+    if (!out) return fail(CONCORD_ERR_ARG, "out is NULL");
+    memset(out, 0, sizeof(*out));
+    if (p < 2 || p > (1LL << 30) || n_sms < 1) return fail(CONCORD_ERR_ARG, "bad p or n_sms");
+    const int ip = (int)p;
+    int w = (ip + n_sms - 1) / n_sms;  // create_common's default single-device slabs, one CTA per SM
+    if (w < 8) w = 8;
+    w = (w + 1) & ~1;
+    const int nblk = (ip + w - 1) / w;
+    const int half = (ip + (ip & 1)) / 2;
+    int share = (half + nblk - 1) / nblk;
+    if (share < WFORM_SHARE_MIN) share = WFORM_SHARE_MIN < half ? WFORM_SHARE_MIN : half;
+    out->slab_width = w;
+    out->ctas = nblk;
+    out->share = share;
+    QbPlan plan;
+    if (ip >= 256 && QB_DEFAULT && qblock_plan(ip, nblk, share, QB_DEFAULT_D, true, &plan)) {
+        out->colours_per_barrier = plan.D;
+        out->cell_buffers = plan.nbuf;
+        out->tdiag_in_smem = plan.td;
+        out->ring_stages = plan.ring;
+        out->smem_bytes = (int64_t)plan.smem;
+    }
+    return CONCORD_OK;
 }
 
 int concord_host_alloc(int64_t bytes, void** out) {
