@@ -213,6 +213,9 @@ struct Smem {
     double* td;     // [p] T diagonal in shared memory (small p), or NULL
 };
 
+// kProf: the phase profiler (CONCORD_PHASE_PROFILE); the production instance carries no timers.
+template <bool kProf>
+#define PCLK() (kProf ? clock64() : 0ll)
 __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_epoch;               // chain: last phase g whose barrier was passed
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
     }
     __syncthreads();
 
-    unsigned long long* prof = (a.prof && bl == 0) ? a.prof : nullptr;
+    unsigned long long* prof = (kProf && a.prof && bl == 0) ? a.prof : nullptr;
 
     if (warp < kChainWarps) {
         // ============================================================ chain warps
@@ -331,14 +334,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         int snnz = 0;
         long long t_wait = 0, t_stage = 0, t_work = 0, t_pub = 0, t_share = 0, t_end = 0;
         while (true) {
-            long long t0 = clock64();
+            long long t0 = PCLK();
             if (tc == 0) {
                 const unsigned long long target = a.bar_base + (unsigned long long)(g + 1) * (unsigned long long)nblk;
                 wait_counter(barL, target, a.sys_scope, g, a.hang);
                 st_vol(&s_epoch, g);
             }
             bar_chain();
-            long long t1 = clock64();
+            long long t1 = PCLK();
             t_wait += t1 - t0;
             const double2* __restrict__ pb = pubL + (size_t)(g % 3) * p;
             const size_t pn_off = (size_t)((g + 1) % 3) * p;
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                         if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, g, Q, ld_vol(&s_staged), 0, 0);
                     }
                 }
-                long long t2 = clock64();
+                long long t2 = PCLK();
                 t_stage += t2 - t1;
                 t1 = t2;
                 const double* st = sm.stage + (size_t)slot * ssz;
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 }
             }
 
-            if (tc == 0) t_pub += clock64() - t1;
+            if (tc == 0) t_pub += PCLK() - t1;
             // ---- this CTA's share of the colour's closed forms -> dring + delta list segment
             // (runs on the last chain threads, concurrently with the publishers above)
             const int lslot = g % a.rl;
@@ -494,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     snnz = 0;
                 }
             }
-            if (tc == kChain - 1) t_share += clock64() - t1;
-            const long long tb = clock64();
+            if (tc == kChain - 1) t_share += PCLK() - t1;
+            const long long tb = PCLK();
             bar_chain();
             if (tc == 0) {
                 if (ph < m && b < a.nsh) {
@@ -515,8 +518,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 }
                 arrive_all(a);
             }
-            if (tc == 0) t_end += clock64() - tb;
-            t_work += clock64() - t1;
+            if (tc == 0) t_end += PCLK() - tb;
+            t_work += PCLK() - t1;
             if (ph == m) {
                 ph = 0;
                 ++it;
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         long long t_busy = 0, t_idle = 0, nbatch = 0, t_head = 0, t_diag = 0, t_h0 = 0, t_h1 = 0, t_h2 = 0;
         unsigned long long idle_since = 0;  // watchdog (thread ta == 0)
         while (true) {
-            const long long t0 = clock64();
+            const long long t0 = PCLK();
             bar_apply();  // everyone has consumed the previous broadcast
             if (ta == 0) {
                 s_aE = ld_vol(&s_epoch);
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             const int target = (stopg < 0) ? min(E + a.stage_ahead, C + 1 + lmax) : staged;
             const int nq = max(0, target - staged);
             if (!have && nq == 0) {
-                t_idle += clock64() - t0;
+                t_idle += PCLK() - t0;
                 // the chain stopped after this slab already reached the last phase: done
                 if (stopg >= 0 && C >= stopg) break;
                 if (ta == 0) {
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
             }
             idle_since = 0;
 
-            const long long ta0 = clock64();
+            const long long ta0 = PCLK();
             // ---- one round trip: segment heads (count + first entry) and the stage cells
             for (int idx = ta; idx < nseg; idx += kApply) {
                 const int jb = idx / nsh;
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
                 }
             }
-            const long long ta1 = clock64();
+            const long long ta1 = PCLK();
             for (int idx = ta; idx < nq * wl; idx += kApply) {
                 const int qi = idx / wl, j = idx - qi * wl;
                 const int Q = staged + 1 + qi;
@@ -659,9 +662,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     if (i < L) st[(2 + i) * w + j] = (ys[i] >= 0) ? tv[i] : 0.0;
             }
             for (int Q = staged + 1 + ta; Q <= target; Q += kApply) s_stbase[Q % kSlots] = C;
-            const long long ta2 = clock64();
+            const long long ta2 = PCLK();
             bar_apply();
-            t_head += clock64() - t0;
+            t_head += PCLK() - t0;
             t_h0 += ta0 - t0;
             t_h1 += ta1 - ta0;
             t_h2 += ta2 - ta1;
@@ -762,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 C = k0;
                 cph = m;
                 cit = it0;
-                t_diag += clock64() - t0;
+                t_diag += PCLK() - t0;
             } else if (nb > 0) {
                 // ---- colour phases k0 .. k1
                 int total = 0;
@@ -858,7 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 cit = it0;
                 ++nbatch;
             }
-            t_busy += clock64() - t0;
+            t_busy += PCLK() - t0;
             if (stopg >= 0 && C >= stopg) break;
         }
         if (prof && ta == 0) {
@@ -878,6 +881,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
         a.status[1] = s_conv;
     }
 }
+#undef PCLK
+
 
 // --------------------------------------------------------------- layout kernels
 // Row-major p x p (leading dim ld) -> nblk slabs of width w starting at global
@@ -988,12 +993,12 @@ size_t wform_smem_bytes(int w, int p, int nblk, int lmax) {
 
 cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st) {
     const size_t smem = wform_smem_bytes(args.w, args.p, args.nblk_tot, args.lmax);
-    cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    const void* fn = args.prof ? (const void*)pcd_wform_kernel<true> : (const void*)pcd_wform_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     WformArgs copy = args;
     void* kargs[] = {&copy};
-    return cudaLaunchCooperativeKernel((void*)pcd_wform_kernel, dim3(nblk), dim3(kThreads), kargs, smem, st);
+    return cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(kThreads), kargs, smem, st);
 }
 
 cudaError_t wform_max_blocks(int w, int p, int nblk_tot, int* max_blocks) {
@@ -1002,11 +1007,13 @@ cudaError_t wform_max_blocks(int w, int p, int nblk_tot, int* max_blocks) {
         *max_blocks = 0;
         return cudaSuccess;
     }
-    cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(pcd_wform_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(pcd_wform_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcd_wform_kernel, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcd_wform_kernel<false>, kThreads, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
