@@ -1,28 +1,35 @@
 """Benchmark: CONCORD-PCD on B200 vs the reference CPU path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode path|sharded]
+                    [--concurrency k]
 
 Workload (BASELINE.json configs[2], the paper workload): AR(2) truth,
 p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
-the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = one complete
-cold-start CONCORD-PCD fit (identity init, delta_tol 1e-5) at the next lambda
-of the path; K=10 covers the whole path.  The metric is sweeps/s (outer
-iterations per second, BASELINE "sweeps/sec"), with seconds-to-converge per
-lambda reported beside it.
+the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = the whole path:
+ten complete cold-start CONCORD-PCD fits (identity init, delta_tol 1e-5),
+scheduled by the package's PathScheduler -- --concurrency k (default 2) fits
+at a time, each on its own share of the SMs (own solver, stream and host
+thread), while the fits are sparse (one latency-bound fit leaves most of a
+B200 idle), then one at a time on all SMs once they turn dense.
+--concurrency 1 runs every fit on all SMs.
+The metric is sweeps/s (outer iterations per second, BASELINE "sweeps/sec"),
+with seconds-to-converge per lambda reported beside it.
 
-* value: device time (CUDA events on the solver's stream) with T resident in
-  HBM; the W/T/Omega working set (3 x 200 MB) exceeds the 126 MB L2.
-* e2e: the same metric through the public API `pcd_fit(GramMatrix, SolverConfig)`
-  with T in pinned host memory: every step uploads T (H2D) and reads Omega back (D2H).
-* roofline: the fit kernel's (pcd_qblock_kernel, or pcd_wform_kernel) algorithmic bytes per launch / its event time.
+* value: device time (CUDA events on the solvers' streams, from one start
+  event to the last stream's end) with T resident in HBM; the W/T/Omega
+  working set (3 x 200 MB per solver) exceeds the 126 MB L2.
+* e2e: the same metric through the public API -- `pcd_path(GramMatrix,
+  lambdas, concurrency=k)` -- with T in pinned host memory: every step uploads
+  T (H2D, once per solver) and reads every Omega back (D2H).
+* roofline: the fit kernel's (pcd_qblock_kernel) algorithmic bytes of all
+  fits / the device time of the steps (aggregate over the concurrent fits).
 * cpu_baseline / --impl reference: the reference's own compiled sweep
   (oracle/_ref, built from /root/reference's _ckernels.pyx) on all host cores,
   timed on a bounded sample of rounds (sweep cost is data-independent).
 
 Multi-GPU (torchrun, one rank per GPU):
-* --mode path (default): the lambda path is split over the ranks, each GPU
-  fits its own lambdas (independent problems, no data-path collective;
-  scaling "weak").
+* --mode path (default): every GPU runs the whole path (independent
+  problems, no data-path collective; scaling "weak").
 * --mode sharded: BASELINE configs[3] -- p=20000, n=5000 -- ONE problem
   column-sharded over all ranks (paper_2106_09382_b200.dist): every colour's
   published values are all-gathered in-kernel through NVLink peer stores
@@ -51,13 +58,15 @@ UNIT = "sweeps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["path", "sharded"], default="path")
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--delta-tol", type=float, default=1e-5)
+    ap.add_argument("--concurrency", type=int, default=2,
+                    help="fits run at a time per GPU, each on SMs/k (path mode); 1 = one fit on all SMs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
@@ -248,58 +257,82 @@ def run_ours(args, d):
 
     torch.cuda.set_device(d.local)
     p, n, K, W = args.p, args.n, args.steps, args.warmup
+    k = max(1, int(args.concurrency))
     x = make_problem(p, n)
-    stream = torch.cuda.Stream()
-    s = cb.Solver(p, device=d.local)
-    s.set_stream(stream.cuda_stream)
+    # One step = the whole cold lambda path, run by the package's PathScheduler: k fits at a time,
+    # each on its own share of the SMs (own solver, stream and host thread), while the fits are
+    # sparse (latency-bound: one fit leaves most of a B200 idle); one at a time on all SMs once they
+    # turn dense.  k = 1: every fit on all SMs.
+    sched = cb.PathScheduler(p, device=d.local, k=k)
+    streams = [torch.cuda.Stream() for _ in sched.solvers]
+    for sv, st in zip(sched.solvers, streams):
+        sv.set_stream(st.cuda_stream)
+    s, stream = sched.full, streams[-1]
     lay = s.layout()
     kernel = f"pcd_qblock_kernel (D={lay['kernel']})" if lay["kernel"] else "pcd_wform_kernel"
     g0 = time.perf_counter()
     s.gram_from_data(cb.DataMatrix(x, centered=True))
     gram_s = time.perf_counter() - g0
+    g = s.gram()
+    for sv in sched.shares:
+        sv.set_gram(g)
+    lams = list(LAMS)
 
-    def lam_at(step):
-        return LAMS[(d.rank + step * d.world) % len(LAMS)]
-
-    def one_fit(lam):
-        rc, res, deltas, objs, secs = s.fit_raw(lam, args.delta_tol, 5000, trace=True)
+    def one_fit(sv, lam):
+        rc, res, deltas, objs, secs = sv.fit_raw(lam, args.delta_tol, 5000, trace=True)
         nnz = np.zeros(res.iterations, dtype=np.int64)
         cnt = ctypes_int()
-        _lib.check(_lib.load().concord_solver_sweep_stats(s._h, _lib.ptr(nnz), res.iterations, cnt))
-        return res, nnz
+        _lib.check(_lib.load().concord_solver_sweep_stats(sv._h, _lib.ptr(nnz), res.iterations, cnt))
+        return (lam, int(res.iterations), float(res.kernel_ms), nnz, bool(res.converged), int(res.edge_count),
+                int(res.n_blocks), int(res.slab_width))
+
+    def frac(sv, f):
+        return float(f[3].sum()) / (f[1] * (p * (p - 1) / 2))
+
+    def step(out):
+        out.extend(sched.run(lams, one_fit, frac))
 
     for i in range(W):
-        one_fit(lam_at(i))
+        step([])
     clocks = Clocks(d.local)
     d.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in streams]
     e0.record(stream)
+    for st in streams[:-1]:
+        st.wait_event(e0)
     fits = []
     for i in range(K):
-        lam = lam_at(i)
-        res, nnz = one_fit(lam)
-        fits.append((lam, int(res.iterations), float(res.kernel_ms), nnz, bool(res.converged), int(res.edge_count),
-                     int(res.n_blocks), int(res.slab_width)))
-    e1.record(stream)
+        step(fits)
+    for ev, st in zip(e1, streams):
+        ev.record(st)
     torch.cuda.synchronize()
     d.barrier()
     clk = clocks.stop()
-    elapsed_ms = d.max(e0.elapsed_time(e1))
+    elapsed_ms = d.max(max(e0.elapsed_time(ev) for ev in e1))
     sweeps = d.sum(sum(f[1] for f in fits))
     value = sweeps / (elapsed_ms / 1e3)
 
-    # roofline of the dominant kernel (the fit kernel), per launch
+    # roofline of the dominant kernel (the fit kernel): algorithmic bytes of all fits over the
+    # device time they took (the concurrent fits' launches overlap, so it is aggregate)
     kern_ms = [f[2] for f in fits]
     bytes_per = [algorithmic_bytes(p, f[3]) for f in fits]
     avg_ms = sum(kern_ms) / len(kern_ms)
     avg_bytes = sum(bytes_per) / len(bytes_per)
     peak, peak_src = measured_peak_hbm()
-    achieved = avg_bytes / (avg_ms / 1e3) / 1e9
+    achieved = sum(bytes_per) / (elapsed_ms / 1e3) / 1e9
     workload = f"ar2 p={p} n={n} lambda-path cold"
     traffic = ncu_traffic(workload)
-    nnz_frac = [float(f[3].sum()) / (f[1] * (p * (p - 1) / 2)) for f in fits]
+    nnz_frac = [frac(None, f) for f in fits]
+    nsm = _lib.device_sm_count(d.local)
+    shared = [f[0] for f in fits[:len(lams)] if f[6] < fits[-1][6]] if k > 1 else []
+    par = (f"PathScheduler: {k} concurrent fits on {nsm // k} of {nsm} SMs each (own solver, stream, host "
+           f"thread) while sparse (lambdas {shared}), then one at a time on all SMs" if k > 1 else
+           "one fit at a time on all SMs, persistent cooperative kernel")
+    if d.world > 1:
+        par = f"{d.world} GPU(s), each running the whole path (independent problems); " + par
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
@@ -307,11 +340,10 @@ def run_ours(args, d):
         "dtype": "f64",
         "data": "synthetic: AR(2) truth (datagen.ar2_precision), X ~ N(0, inv(truth)) n=2000 seed 0, centred",
         "config": {"workload": workload, "source": "BASELINE.json configs[2] (paper workload)", "p": p, "n": n,
-                   "lambdas": [lam_at(i) for i in range(K)], "delta_tol": args.delta_tol, "init": "identity",
+                   "lambdas": lams, "fits_per_step": len(lams), "concurrency": k, "delta_tol": args.delta_tol,
+                   "init": "identity",
                    "l2": "inputs larger than L2 (T, W, Omega slabs 3 x %.0f MB > 126 MB)" % (8 * p * p / 1e6),
-                   "parallelism": f"{d.world} GPU(s), independent lambda fits per GPU" if d.world > 1 else
-                   "1 GPU, persistent cooperative kernel", "kernel": kernel, "n_blocks": fits[0][6],
-                   "slab_width": fits[0][7]},
+                   "parallelism": par, "kernel": kernel, "n_blocks": fits[0][6], "slab_width": fits[0][7]},
         "seconds_to_converge": {f"{f[0]:.2f}": round(f[2] / 1e3, 6) for f in fits},
         "iterations": {f"{f[0]:.2f}": f[1] for f in fits},
         "edges": {f"{f[0]:.2f}": f[5] for f in fits},
@@ -320,13 +352,15 @@ def run_ours(args, d):
         "roofline": {"kernel": kernel, "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
-                     "note": "bytes = sum over sweeps of 48p*nnz_k per colour + 24p per colour + 32p^2 diag/objective"},
-        "gpu_launches": 3 * K,
+                     "note": "bytes = sum over sweeps of 48p*nnz_k per colour + 24p per colour + 32p^2 diag/objective"
+                             + "; achieved = all fits' bytes / the device time of the steps (aggregate over "
+                             "concurrent fits)"},
+        "gpu_launches": 3 * len(fits),
         "clocks": clk,
     }
 
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, d, s, stream, lam_at)
+        out["e2e"] = run_e2e(args, d, s, stream, lams, k)
     if not args.no_cpu and d.world == 1 and d.rank == 0:
         t_host = s.gram().t
         rate, kind, rounds, el = cpu_reference_rate(t_host, n, 0.3, args.cpu_seconds, os.cpu_count())
@@ -345,8 +379,10 @@ def ctypes_int():
     return ctypes.byref(ctypes.c_int32(0))
 
 
-def run_e2e(args, d, s, stream, lam_at):
-    """Same metric through pcd_fit(GramMatrix host, SolverConfig): H2D T + fit + D2H Omega per step."""
+def run_e2e(args, d, s, stream, lams, k=1):
+    """Same metric through the public API with T in pinned host memory, one step = the whole
+    path: pcd_path(GramMatrix(pinned T), lambdas, concurrency=k) uploads T to each of its solvers
+    (H2D) and returns every Omega (D2H)."""
     import torch
 
     import paper_2106_09382_b200 as cb
@@ -356,24 +392,31 @@ def run_e2e(args, d, s, stream, lam_at):
     t_pinned = _lib.pinned_empty((p, p))
     t_pinned[...] = s.gram().t
     gram = cb.GramMatrix(t_pinned, n)  # validated once, as a user would construct it
+
+    def one_step():
+        reps = cb.pcd_path(gram, lams, delta_tol=args.delta_tol, max_outer_iterations=5000, device=d.local,
+                           concurrency=k)
+        return sum(r.iterations for r in reps)
+
     for i in range(min(W, 2)):
-        cb.pcd_fit(gram, cb.SolverConfig(lam=lam_at(i), max_outer_iterations=5000), device=d.local)
+        one_step()
     d.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     sweeps = 0
     for i in range(K):
-        rep = cb.pcd_fit(gram, cb.SolverConfig(lam=lam_at(i), max_outer_iterations=5000), device=d.local)
-        sweeps += rep.iterations
+        sweeps += one_step()
     e1.record()
     torch.cuda.synchronize()
     d.barrier()
     el = d.max(e0.elapsed_time(e1))
     total = d.sum(sweeps)
-    return {"value": total / (el / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * p * p,
-            "d2h_bytes_per_step": 8 * p * p, "ms_per_step": el / K,
-            "path": "paper_2106_09382_b200.pcd_fit(GramMatrix(pinned T), SolverConfig(lam)) -> FitReport"}
+    nsolvers = (k + 1) if k > 1 else 1
+    return {"value": total / (el / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * p * p * nsolvers,
+            "d2h_bytes_per_step": 8 * p * p * len(lams), "ms_per_step": el / K,
+            "path": f"paper_2106_09382_b200.pcd_path(GramMatrix(pinned T), {len(lams)} lambdas, concurrency={k}) "
+                    "-> FitReports"}
 
 
 def run_sharded(args, d):

@@ -169,6 +169,11 @@ typedef struct {
 } concord_blocked_plan_t;
 int concord_blocked_plan(int64_t p, int32_t n_sms, concord_blocked_plan_t* out);
 
+/* Streaming multiprocessors of a device: a caller running k independent fits concurrently
+ * (e.g. the cold fits of a lambda path) gives each a solver of n_blocks = SMs / k, on its own
+ * stream.  No reference counterpart. */
+int concord_device_sm_count(int32_t device, int32_t* out);
+
 int concord_host_alloc(int64_t bytes, void** out);
 int concord_host_free(void* ptr);
 

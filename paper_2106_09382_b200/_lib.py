@@ -32,7 +32,7 @@ EXPORTS = (
     "concord_solver_create_sharded", "concord_solver_layout", "concord_shard_create",
     "concord_shard_ipc_handle", "concord_shard_open_peers", "concord_solver_objective_parts",
     "concord_solver_check_optimality", "concord_solver_estimate_entries",
-    "concord_ar2_data_f64", "concord_solver_gram_from_ar2", "concord_blocked_plan",
+    "concord_ar2_data_f64", "concord_solver_gram_from_ar2", "concord_blocked_plan", "concord_device_sm_count",
 )
 
 ABI_VERSION = 2
@@ -138,6 +138,7 @@ def load(build_if_missing=True):
             "concord_solver_sweep_stats": ([vp, vp, i32, ctypes.POINTER(i32)], ctypes.c_int),
             "concord_host_alloc": ([i64, ctypes.POINTER(vp)], ctypes.c_int),
             "concord_blocked_plan": ([i64, i32, ctypes.POINTER(BlockedPlan)], ctypes.c_int),
+            "concord_device_sm_count": ([i32, ctypes.POINTER(i32)], ctypes.c_int),
             "concord_host_free": ([vp], ctypes.c_int),
             "concord_gram_f64": ([vp, i64, i64, vp, i32], ctypes.c_int),
             "concord_pcd_fit": ([vp, i64, d, ctypes.POINTER(FitParams), vp, ctypes.POINTER(FitResult), vp, vp,
@@ -221,7 +222,7 @@ class _PooledOwner:
     def __del__(self):
         try:
             free = _POOL.setdefault(self.nbytes, [])
-            if len(free) < _POOL_KEEP:
+            if (len(free) + 1) * self.nbytes <= _POOL_KEEP_BYTES or not free:
                 free.append(self.addr)
             else:
                 load().concord_host_free(ctypes.c_void_p(self.addr))
@@ -230,7 +231,13 @@ class _PooledOwner:
 
 
 _POOL = {}  # nbytes -> free page-locked blocks
-_POOL_KEEP = 4
+_POOL_KEEP_BYTES = 4 << 30  # per block size (a lambda path keeps ten 200 MB results alive at p=5000)
+
+
+def device_sm_count(device=0):
+    n = ctypes.c_int32()
+    check(load().concord_device_sm_count(int(device), ctypes.byref(n)))
+    return n.value
 
 
 def blocked_plan(p, n_sms=148):

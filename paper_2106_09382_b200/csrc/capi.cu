@@ -443,7 +443,9 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
     CKC(cudaStreamSynchronize(s->stream));
 #undef CKC
     // temporally blocked chain for the single-device unsharded solver
-    bool use_qb = (G == 1 && rank < 0 && n_blocks <= 0 && ip >= 256);
+    // the blocked kernel for single-device solvers (also with an explicit slab count: a fit on a
+    // share of the SMs, e.g. concurrent lambda fits); CONCORD_KERNEL=wform selects the per-phase one
+    bool use_qb = (G == 1 && rank < 0 && ip >= 256);
     if (const char* e = getenv("CONCORD_KERNEL")) use_qb = use_qb && strcmp(e, "qblock") == 0;
     else use_qb = use_qb && QB_DEFAULT;
     if (use_qb) {
@@ -1043,6 +1045,15 @@ int concord_solver_gram_from_ar2(concord_solver* s, int64_t n, uint64_t seed) {
     if (!rc) rc = concord_solver_gram_from_data(s, X, n, CONCORD_DEVICE);
     cudaFree(X);
     return rc;
+}
+
+int concord_device_sm_count(int32_t device, int32_t* out) {
+    if (!out) return fail(CONCORD_ERR_ARG, "out is NULL");
+    *out = 0;
+    int n = 0;
+    CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    *out = n;
+    return CONCORD_OK;
 }
 
 int concord_blocked_plan(int64_t p, int32_t n_sms, concord_blocked_plan_t* out) {

@@ -34,6 +34,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "pcd_wform.h"
 
@@ -1412,11 +1414,24 @@ int qblock_colour_warps(int share, int D) { return qb::colour_warps(share, D); }
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
     const size_t smem = qblock_smem_bytes(args.p, nblk, args.share, args.D, args.tdiag_smem, args.nbuf, args.ring_stages);
     const void* fn = args.prof ? (const void*)qb::pcd_qblock_kernel<true> : (const void*)qb::pcd_qblock_kernel<false>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    {
+        // raise the kernel's shared-memory limit only when needed: setting a function attribute
+        // while another fit runs the kernel on another stream serialises the two
+        static std::mutex mu;
+        static size_t set_bytes[2] = {0, 0};
+        std::lock_guard<std::mutex> lock(mu);
+        size_t& cur = set_bytes[args.prof ? 1 : 0];
+        if (smem > cur) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            cur = smem;
+        }
+    }
+    cudaError_t e;
     QbArgs copy = args;
     void* kargs[] = {&copy};
-    return cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(qb::kThreads), kargs, smem, st);
+    e = cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(qb::kThreads), kargs, smem, st);
+    return e;
 }
 
 }  // namespace concord

@@ -356,3 +356,22 @@ def test_result_arrays_are_independent_pinned_pool(golden):
         assert np.array_equal(r1.estimate.omega, keep)
         r4 = s.fit(0.1, 1e-5, 5000)
         assert_close_support(r4.estimate.omega, c["omega"])
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_concurrent_lambda_path_equals_sequential_fits(k):
+    """pcd_path(concurrency=k) (PathScheduler): k cold fits at a time on SMs/k slabs each, own
+    stream and thread, while sparse, then one at a time on all SMs -- the same bits and iteration
+    counts as one fit at a time on all SMs."""
+    _, t = synth.problem("ar2", 1000, 400, seed=7)
+    g = cb.GramMatrix(t, 400)
+    lams = [0.4, 0.3, 0.2, 0.15, 0.1]
+    seq = cb.pcd_path(g, lams, max_outer_iterations=300)
+    con = cb.pcd_path(g, lams, max_outer_iterations=300, concurrency=k)
+    assert len(con) == len(lams)
+    for a, b in zip(seq, con):
+        assert a.iterations == b.iterations
+        assert np.array_equal(a.estimate.omega, b.estimate.omega)
+        np.testing.assert_allclose(a.objective_trace, b.objective_trace, rtol=1e-12)
+    with pytest.raises(ValueError):
+        cb.pcd_path(g, lams, warm_start=True, concurrency=k)
