@@ -7,11 +7,11 @@ Workload (BASELINE.json configs[2], the paper workload): AR(2) truth,
 p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
 the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = the whole path:
 ten complete cold-start CONCORD-PCD fits (identity init, delta_tol 1e-5),
-scheduled by the package's PathScheduler -- --concurrency k (default 2) fits
-at a time, each on its own share of the SMs (own solver, stream and host
-thread), while the fits are sparse (one latency-bound fit leaves most of a
-B200 idle), then one at a time on all SMs once they turn dense.
---concurrency 1 runs every fit on all SMs.
+scheduled by the package's PathScheduler -- --concurrency k (default 2)
+lanes, each a solver on its own share of the SMs (own stream and host
+thread), pull the fits densest first (one latency-bound fit leaves most of a
+B200 idle; longest job first balances the lanes).  --concurrency 1 runs every
+fit on all SMs, one after the other.
 The metric is sweeps/s (outer iterations per second, BASELINE "sweeps/sec"),
 with seconds-to-converge per lambda reported beside it.
 
@@ -259,10 +259,9 @@ def run_ours(args, d):
     p, n, K, W = args.p, args.n, args.steps, args.warmup
     k = max(1, int(args.concurrency))
     x = make_problem(p, n)
-    # One step = the whole cold lambda path, run by the package's PathScheduler: k fits at a time,
-    # each on its own share of the SMs (own solver, stream and host thread), while the fits are
-    # sparse (latency-bound: one fit leaves most of a B200 idle); one at a time on all SMs once they
-    # turn dense.  k = 1: every fit on all SMs.
+    # One step = the whole cold lambda path, run by the package's PathScheduler: k lanes, each a
+    # solver on its own share of the SMs (own stream and host thread), pull the fits densest first
+    # (one latency-bound fit leaves most of a B200 idle).  k = 1: every fit on all SMs.
     sched = cb.PathScheduler(p, device=d.local, k=k)
     streams = [torch.cuda.Stream() for _ in sched.solvers]
     for sv, st in zip(sched.solvers, streams):
@@ -290,7 +289,7 @@ def run_ours(args, d):
         return float(f[3].sum()) / (f[1] * (p * (p - 1) / 2))
 
     def step(out):
-        out.extend(sched.run(lams, one_fit, frac))
+        out.extend(sched.run(lams, one_fit))
 
     for i in range(W):
         step([])
@@ -327,9 +326,8 @@ def run_ours(args, d):
     traffic = ncu_traffic(workload)
     nnz_frac = [frac(None, f) for f in fits]
     nsm = _lib.device_sm_count(d.local)
-    shared = [f[0] for f in fits[:len(lams)] if f[6] < fits[-1][6]] if k > 1 else []
-    par = (f"PathScheduler: {k} concurrent fits on {nsm // k} of {nsm} SMs each (own solver, stream, host "
-           f"thread) while sparse (lambdas {shared}), then one at a time on all SMs" if k > 1 else
+    par = (f"PathScheduler: {k} lanes of {nsm // k} of {nsm} SMs each (own solver, stream, host thread) "
+           f"pulling the path's fits densest first; each fit a persistent cooperative kernel" if k > 1 else
            "one fit at a time on all SMs, persistent cooperative kernel")
     if d.world > 1:
         par = f"{d.world} GPU(s), each running the whole path (independent problems); " + par

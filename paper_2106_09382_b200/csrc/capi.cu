@@ -776,8 +776,11 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     s->it_base += iters;
     std::vector<double> dl(iters > 0 ? iters : 1);
     std::vector<unsigned long long> tm(iters + 1);
-    CK(cudaMemcpy(dl.data(), s->rec_delta, sizeof(double) * iters, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(tm.data(), s->rec_time, sizeof(unsigned long long) * (iters + 1), cudaMemcpyDeviceToHost));
+    // on the solver's stream: a legacy-stream copy could wait for another solver's running fit
+    CK(cudaMemcpyAsync(dl.data(), s->rec_delta, sizeof(double) * iters, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(tm.data(), s->rec_time, sizeof(unsigned long long) * (iters + 1), cudaMemcpyDeviceToHost,
+                       s->stream));
+    CK(cudaStreamSynchronize(s->stream));
     if (delta_trace)
         for (int i = 0; i < iters; ++i) delta_trace[i] = dl[i];
     if (sweep_seconds)
@@ -785,7 +788,8 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     if (objective_trace) {
         if (prm->want_trace) {
             std::vector<double> ro((size_t)iters * s->nblk_launch * 3);
-            CK(cudaMemcpy(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost, s->stream));
+            CK(cudaStreamSynchronize(s->stream));
             for (int i = 0; i < iters; ++i) {
                 double q = 0.0, pen = 0.0, lg = 0.0;
                 for (int b = 0; b < s->nblk_launch; ++b) {
@@ -859,7 +863,10 @@ int concord_solver_objective_parts(concord_solver* s, double* parts, int32_t cap
     DeviceGuard g(s->dev);
     const int k = s->last_iters < cap ? s->last_iters : cap;
     std::vector<double> ro((size_t)k * s->nblk_launch * 3);
-    if (k > 0) CK(cudaMemcpy(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost));
+    if (k > 0) {
+        CK(cudaMemcpyAsync(ro.data(), s->rec_obj, sizeof(double) * ro.size(), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
     for (int i = 0; i < k; ++i) {
         double q = 0.0, pen = 0.0, lg = 0.0;
         for (int b = 0; b < s->nblk_launch; ++b) {
@@ -896,7 +903,10 @@ int concord_solver_sweep_stats(concord_solver* s, int64_t* nnz_pairs, int32_t ca
     if (!s || !count) return fail(CONCORD_ERR_ARG, "NULL argument");
     DeviceGuard g(s->dev);
     const int k = s->last_iters < cap ? s->last_iters : cap;
-    if (k > 0 && nnz_pairs) CK(cudaMemcpy(nnz_pairs, s->rec_nnz, sizeof(int64_t) * k, cudaMemcpyDeviceToHost));
+    if (k > 0 && nnz_pairs) {
+        CK(cudaMemcpyAsync(nnz_pairs, s->rec_nnz, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
     *count = s->last_iters;
     return CONCORD_OK;
 }

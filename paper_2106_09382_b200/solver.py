@@ -317,9 +317,9 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
     estimate (SolverConfig.init semantics).  Returns one FitReport per lambda
     (a non-converged fit is returned with converged=False, not raised).
 
-    concurrency=k (cold mode) runs k fits at a time, each on its own share of
-    the SMs, while the fits are sparse, then one at a time on all SMs
-    (`PathScheduler`); the results are bitwise those of sequential fits.
+    concurrency=k (cold mode) runs the fits on k lanes, each a solver on its
+    own share of the SMs, densest lambda first (`PathScheduler`); the results
+    are bitwise those of sequential fits.
     """
     if concurrency > 1:
         if warm_start:
@@ -342,19 +342,19 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
 
 
 class PathScheduler:
-    """Cold lambda path on one device: k fits at a time while the fits are sparse, then one at a
-    time on all SMs.
+    """Cold lambda path on one device: k lanes, each a solver on its own share of the SMs.
 
-    A sparse fit is latency-bound: one fit leaves most of a B200 idle, and k fits on SMs/k slabs
-    each (own solver, stream and host thread) finish ~1.6x sooner at k=2 (p=5000).  A dense fit is
-    bandwidth-bound and slower on a share of the device, so once a group's densest fit moved more
-    than `dense_switch` of the pairs per sweep, the remaining lambdas (a descending path only gets
-    denser) run one at a time on a full-device solver.  Results are bitwise those of sequential
+    A sparse fit is latency-bound: one fit leaves most of a B200 idle, and two fits on halves of
+    the device (own solver, stream and host thread) finish ~1.6x sooner than one after the other
+    on all of it; two dense fits still gain ~1.2x.  The fits of a path are independent, so the
+    path is a scheduling problem: the lanes pull the next lambda from one queue, densest (smallest
+    lambda) first -- longest job first, so the long dense fit overlaps with the many short sparse
+    ones.  A single fit runs on a full-device solver.  Results are bitwise those of sequential
     fits: the slab count never changes the bits.
     """
 
-    def __init__(self, p, device=0, k=2, dense_switch=0.003):
-        self.p, self.device, self.k, self.dense_switch = int(p), int(device), int(k), float(dense_switch)
+    def __init__(self, p, device=0, k=2):
+        self.p, self.device, self.k = int(p), int(device), int(k)
         nb = max(1, _lib.device_sm_count(device) // self.k) if self.k > 1 else 0
         self.shares = [Solver(p, device=device, n_blocks=nb) for _ in range(self.k)] if self.k > 1 else []
         self.full = Solver(p, device=device)
@@ -371,39 +371,38 @@ class PathScheduler:
         for s in self.solvers:
             s.set_gram(gram)
 
-    def run(self, lams, fit_one, moving_fraction):
-        """fit_one(solver, lam) -> result; moving_fraction(solver, result) -> fraction of the pairs
-        that moved per sweep.  Returns the results in lambda order."""
+    def run(self, lams, fit_one):
+        """fit_one(solver, lam) -> result; returns the results in the order of `lams`."""
         import threading
 
         lams = list(lams)
         out = [None] * len(lams)
-        i, shared = 0, self.k > 1
-        while i < len(lams):
-            if not shared:
-                out[i] = fit_one(self.full, lams[i])
-                i += 1
-                continue
-            group = list(range(i, min(i + self.k, len(lams))))
-            errors, fracs = [], [0.0] * len(group)
+        if self.k <= 1 or len(lams) <= 1:
+            for i, lam in enumerate(lams):
+                out[i] = fit_one(self.full, lam)
+            return out
+        queue = sorted(range(len(lams)), key=lambda i: lams[i])  # densest first
+        lock = threading.Lock()
+        errors = []
 
-            def work(j, idx):
-                try:
-                    out[idx] = fit_one(self.shares[j], lams[idx])
-                    fracs[j] = moving_fraction(self.shares[j], out[idx])
-                except BaseException as e:  # re-raised in the caller's thread
-                    errors.append(e)
+        def lane(j):
+            try:
+                while True:
+                    with lock:
+                        if not queue or errors:
+                            return
+                        i = queue.pop(0)
+                    out[i] = fit_one(self.shares[j], lams[i])
+            except BaseException as e:  # re-raised in the caller's thread
+                errors.append(e)
 
-            threads = [threading.Thread(target=work, args=(j, idx)) for j, idx in enumerate(group)]
-            for t in threads:
-                t.start()
-            for t in threads:
-                t.join()
-            if errors:
-                raise errors[0]
-            if max(fracs) > self.dense_switch:
-                shared = False
-            i += len(group)
+        threads = [threading.Thread(target=lane, args=(j,)) for j in range(self.k)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
         return out
 
 
@@ -423,8 +422,7 @@ def _path_concurrent(x_or_gram, lams, delta_tol, max_outer_iterations, device, t
         _POOL[key] = sched
     sched.set_gram(gram)
     return sched.run(lams, lambda s, lam: s.fit(lam, delta_tol, max_outer_iterations, trace=trace,
-                                                raise_on_cap=False),
-                     lambda s, rep: s.moving_fraction())
+                                                raise_on_cap=False))
 
 
 def _gram_p(x):
