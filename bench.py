@@ -7,10 +7,10 @@ Workload (BASELINE.json configs[2], the paper workload): AR(2) truth,
 p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
 the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = the whole path:
 ten complete cold-start CONCORD-PCD fits (identity init, delta_tol 1e-5),
-scheduled by the package's PathScheduler -- --concurrency k (default 2)
-lanes, each a solver on its own share of the SMs (own stream and host
-thread), pull the fits densest first (one latency-bound fit leaves most of a
-B200 idle; longest job first balances the lanes).  --concurrency 1 runs every
+scheduled by the package's PathScheduler -- --concurrency k (default 3)
+lanes, each a solver on its own share of the SMs (k=3: 74/37/37; own stream
+and host thread), pull the fits densest first (one latency-bound fit leaves
+most of a B200 idle; longest job first balances the lanes).  --concurrency 1 runs every
 fit on all SMs, one after the other.
 The metric is sweeps/s (outer iterations per second, BASELINE "sweeps/sec"),
 with seconds-to-converge per lambda reported beside it.
@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--delta-tol", type=float, default=1e-5)
-    ap.add_argument("--concurrency", type=int, default=2,
+    ap.add_argument("--concurrency", type=int, default=3,
                     help="fits run at a time per GPU, each on SMs/k (path mode); 1 = one fit on all SMs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -326,8 +326,9 @@ def run_ours(args, d):
     traffic = ncu_traffic(workload)
     nnz_frac = [frac(None, f) for f in fits]
     nsm = _lib.device_sm_count(d.local)
-    par = (f"PathScheduler: {k} lanes of {nsm // k} of {nsm} SMs each (own solver, stream, host thread) "
-           f"pulling the path's fits densest first; each fit a persistent cooperative kernel" if k > 1 else
+    par = (f"PathScheduler: {k} lanes of {'/'.join(str(v) for v in sched.lanes)} of {nsm} SMs (own solver, "
+           f"stream, host thread) pulling the path's fits densest first; each fit a persistent cooperative "
+           f"kernel" if k > 1 else
            "one fit at a time on all SMs, persistent cooperative kernel")
     if d.world > 1:
         par = f"{d.world} GPU(s), each running the whole path (independent problems); " + par

@@ -6,7 +6,9 @@ import paper_2106_09382_b200 as cb
 from paper_2106_09382_b200 import synth
 p, n = 5000, 2000
 x = synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
-sched = cb.PathScheduler(p, k=2)
+import os
+lanes = [int(v) for v in os.environ.get('LANES', '74,74').split(',')]
+sched = cb.PathScheduler(p, lanes=lanes)
 sched.full.gram_from_data(cb.DataMatrix(x, centered=True))
 g = sched.full.gram()
 for s in sched.shares:
@@ -20,7 +22,7 @@ def fit_one(s, lam):
     t1 = time.perf_counter() - t00[0]
     log.append((threading.current_thread().name, lam, round(t0, 3), round(t1, 3), round(res.kernel_ms / 1e3, 3)))
     return res
-for rep in range(3):
+for rep in range(2):
     log.clear()
     t00[0] = time.perf_counter()
     sched.run(lams, fit_one)
