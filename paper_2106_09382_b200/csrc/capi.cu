@@ -328,6 +328,12 @@ int setup_qblock(concord_solver* s) {
     s->qb_nbuf = plan.nbuf;
     s->qb_td = plan.td;
     s->qb_ring = plan.ring;
+    if (const char* e = getenv("CONCORD_QB_RING")) {  // tuning: a deeper ring when it still fits
+        const int r = atoi(e);
+        if ((r == 2 || r == 4 || r == 6 || r == 8) &&
+            qblock_smem_bytes(p, s->nblk_tot, s->share, plan.D, plan.td, plan.nbuf, r) + 2048 <= 227 * 1024)
+            s->qb_ring = r;
+    }
     s->qb_D = D;
     s->qb_NB = (m + 1 + D - 1) / D;
     s->qb_sr = 4 * D + 4;

@@ -266,13 +266,14 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
         si = (si + 1 == S) ? 0 : si + 1;
     };
     // prologue: S - 1 items in flight; then one issue per completed item, and in the
-    // tail (nothing left to issue) wait for everything.  S is 2, 4 or 6 (shared-memory budget).
+    // tail (nothing left to issue) wait for everything.  S is 2, 4, 6 or 8 (shared-memory budget).
     int ni = min(nmine, S - 1);
     for (int i = 0; i < ni; ++i) issue(i);
     for (int j = 0; j < nmine; ++j) {
         if (ni < nmine) {
             issue(ni++);
-            if (S == 6) asm volatile("cp.async.wait_group 5;" ::: "memory");
+            if (S == 8) asm volatile("cp.async.wait_group 7;" ::: "memory");
+            else if (S == 6) asm volatile("cp.async.wait_group 5;" ::: "memory");
             else if (S == 4) asm volatile("cp.async.wait_group 3;" ::: "memory");
             else asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
