@@ -375,17 +375,27 @@ class PathScheduler:
             raise ValueError(f"lanes {lanes} do not fit the device's {nsm} SMs")
         self.p, self.device, self.k, self.lanes = int(p), int(device), len(lanes), lanes
         self.shares = [Solver(p, device=device, n_blocks=v) for v in lanes] if len(lanes) > 1 else []
-        self.full = Solver(p, device=device)
+        self._full = None  # all-SM solver, created when a path has a single fit (or k <= 1)
+        self._gram = None
+
+    @property
+    def full(self):
+        if self._full is None:
+            self._full = Solver(self.p, device=self.device)
+            if self._gram is not None:
+                self._full.set_gram(self._gram)
+        return self._full
 
     @property
     def solvers(self):
-        return self.shares + [self.full]
+        return self.shares + ([self._full] if self._full is not None else [])
 
     def close(self):
         for s in self.solvers:
             s.close()
 
     def set_gram(self, gram):
+        self._gram = gram
         for s in self.solvers:
             s.set_gram(gram)
 
