@@ -373,8 +373,21 @@ class PathScheduler:
         lanes = sorted((int(v) for v in lanes), reverse=True)
         if sum(lanes) > nsm or any(v < 1 for v in lanes):
             raise ValueError(f"lanes {lanes} do not fit the device's {nsm} SMs")
+        self.shares = []
+        if len(lanes) > 1:
+            try:
+                for v in lanes:
+                    self.shares.append(Solver(p, device=device, n_blocks=v))
+            except _lib.ConcordError as e:
+                # every lane holds its own T, W and Omega (3 x 8p^2 bytes): when they do not fit
+                # (p=50000: 60 GB each), the path runs one fit at a time on all SMs
+                for s in self.shares:
+                    s.close()
+                self.shares = []
+                if getattr(e, "code", None) != _lib.CONCORD_ERR_OOM:
+                    raise
+                lanes = []
         self.p, self.device, self.k, self.lanes = int(p), int(device), len(lanes), lanes
-        self.shares = [Solver(p, device=device, n_blocks=v) for v in lanes] if len(lanes) > 1 else []
         self._full = None  # all-SM solver, created when a path has a single fit (or k <= 1)
         self._gram = None
 

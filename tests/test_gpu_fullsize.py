@@ -98,3 +98,14 @@ def test_largest_config_runs_the_blocked_kernel():
     """configs[4] (p=50000) must fit the blocked kernel's shared-memory plan."""
     with cb.Solver(50000) as s:
         assert s.layout()["kernel"] == 4
+
+
+def test_path_scheduler_lanes_fall_back_when_memory_is_short():
+    """Three lanes at p=50000 need 3 x 60 GB of slabs: the scheduler falls back to one fit at a
+    time on all SMs instead of failing (or keeps every lane when they do fit)."""
+    sched = cb.PathScheduler(50000, k=3)
+    try:
+        assert sched.k in (0, 3)
+        assert len(sched.shares) == (3 if sched.k == 3 else 0)
+    finally:
+        sched.close()
