@@ -1125,18 +1125,20 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const size_t so = (size_t)(Q % a.sr) * p + c;
                     a.stW[so] = val;
                     a.stO[so] = om;
-                    // T entries of the block's earlier phases (kb.ph0 .. ph-1), for the chain's in-block FMAs
-                    int y = circle_partner(x, kb.ph0, m);
-                    for (int ii = 0; ii < i; ++ii) {
-                        a.stT[((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = (y < p) ? __ldcg(Tb + (long long)y * w + j) : 0.0;
-                        if (x == 0) {
-                            y = (y == 1) ? m : y - 1;
-                        } else {
-                            int yy = (y == 0) ? x : y;
-                            yy -= 2;
-                            if (yy < 1) yy += m;
-                            y = (yy == x) ? 0 : yy;
+                    // T entries of the block's earlier phases (kb.ph0 .. ph-1), for the chain's in-block
+                    // FMAs: all loads first (predicated, back to back), then the stores
+                    {
+                        double tv[kDMax - 1];
+                        PartnerWalk pt(x, kb.ph0, m);
+#pragma unroll
+                        for (int ii = 0; ii < kDMax - 1; ++ii) {
+                            const int y = pt.y();
+                            tv[ii] = ldcg_if(Tb + (long long)min(y, p - 1) * w + j, ii < i && y < p);
+                            pt.next();
                         }
+#pragma unroll
+                        for (int ii = 0; ii < kDMax - 1; ++ii)
+                            if (ii < i) a.stT[((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = tv[ii];
                     }
                 }
                 t_stage += PCLK() - ts;
