@@ -14,22 +14,27 @@
 //
 // Per block of D phases (blocks never straddle a sweep; the diagonal phase
 // closes the sweep's last block):
-//  * chain warps: read every cell W[x,c] / Om[x,c] the block's pairs (and
-//    halo) need from the STAGE -- written in global memory by the slab owners
-//    two blocks ahead, already brought forward to the start of the block
-//    before last -- apply the deltas of the two previous blocks (the per-row
-//    delta ring; T entries fetched only where a delta is non-zero) and then,
-//    colour by colour in shared memory, the deltas of this block (T entries
-//    preloaded).  Own pairs write the delta ring and the non-zero delta list;
-//    the diagonal phase writes the (delta, new) vector.  One arrive per block.
-//  * apply warps (as pcd_wform.cu): stream the delta lists into the own slab
-//    in phase order, run the dense diagonal step, and stage the cells of the
-//    block after next at watermark C' = (start of the block before it) - 1,
-//    bringing them forward from their own watermark with exactly the FMAs
-//    they will apply to the slab.
+//  * chain warps.  The cells W[x,c] / Om[x,c] the block's pairs (and halo) need
+//    come from the STAGE, written in global memory by the slab owners with
+//    watermark C'(B) = (start of block B-3) - 1.  Part A of a block's cells --
+//    stage values, in-block T entries, pair slots, the deltas of blocks B-3 and
+//    B-2 (per-row delta ring; T entries only where a delta is non-zero) -- is
+//    built by the chain warps the colours leave free (the prefetch group) while
+//    block B-1's colours run, into the second of two cell buffers.  After the
+//    barrier, part B folds in block B-1's deltas; then the colours run one after
+//    another in shared memory with the block's own deltas; one pass publishes
+//    the own pairs' delta ring and non-zero delta lists; the diagonal phase
+//    writes the (delta, new) vector.  One arrive per block, once the block after
+//    next is staged.
+//  * apply warps (as pcd_wform.cu): stream the delta lists into the own slab in
+//    phase order through a per-thread cp.async ring (per-row chains where a
+//    batch moves a row more than once), run the dense diagonal step, and stage
+//    the cells of upcoming blocks, bringing them forward from their own
+//    watermark with exactly the FMAs they will apply to the slab.
 //
 // Every published value is thus the value of the sequential W-form (same
 // FMAs, same order), and the results equal pcd_wform.cu's bit for bit.
+// Shared-memory plan (cell buffers, T diagonal, ring depth) per p: capi.cu.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -50,7 +55,6 @@ constexpr int kApplyWarps = kApply / 32;
 constexpr int kPairCap = WFORM_PAIR_CAP;
 constexpr int kBatch = WFORM_BATCH;
 constexpr int kUnroll = 2;
-constexpr int kRowUnroll = 2;
 constexpr int kDMax = QB_DMAX;
 constexpr int kChainN = 32;   // batches with row conflicts up to this many entries: per-row chains
 
@@ -112,15 +116,6 @@ __device__ __forceinline__ double ldcg_if(const double* ptr, bool on) {
     return v;
 }
 
-// Pair index of id x in round k (position 0 and m form pair 0; position i pairs with m - i).
-__device__ __forceinline__ int pair_of(int x, int k, int m) {
-    if (x == 0) return 0;
-    int pos = x - 1 + k;
-    pos = 1 + (pos >= m ? pos % m : pos);
-    if (pos == m) return 0;
-    return pos < m - pos ? pos : m - pos;
-}
-
 // Geometry of global block b: first global phase g0, its phase-in-sweep ph0, length len.
 struct Blk {
     int g0, ph0, len, sweep;
@@ -179,57 +174,14 @@ __device__ int apply_scan(int* s, int n, int ta, int* s_wsum) {
     return total;
 }
 
-// Row streams of delta-list entries [e_lo, e_hi) (shared-memory indices; only
-// batch phase `only` when only >= 0): W[dst, own] = fma(d, T[src, own], W[dst, own])
-// for both rows of every pair.
-__device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, const int* L_ph, int only, int e_lo,
-                                           int e_hi, int w2, double* __restrict__ Wb, const double* __restrict__ Tb,
-                                           int ta) {
-    const int w = 2 * w2;
-    const int per = 2 * w2;
-    const int items = (e_hi - e_lo) * per;
-    for (int base = 0; base < items; base += kApply * kRowUnroll) {
-        double2 tv[kRowUnroll], wv[kRowUnroll];
-        double2* wp[kRowUnroll];
-        double dd[kRowUnroll];
-#pragma unroll
-        for (int u = 0; u < kRowUnroll; ++u) {
-            const int idx = base + u * kApply + ta;
-            wp[u] = nullptr;
-            if (idx < items) {
-                const int e = e_lo + idx / per;
-                if (only < 0 || L_ph[e] == only) {
-                    const int rem = idx - (idx / per) * per;
-                    const int h = rem >= w2;
-                    const int j2 = rem - h * w2;
-                    const int2 rs = L_rs[e];
-                    dd[u] = L_d[e];
-                    const int dst = h ? rs.y : rs.x;
-                    const int src = h ? rs.x : rs.y;
-                    wp[u] = reinterpret_cast<double2*>(Wb + (long long)dst * w) + j2;
-                    tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
-                    wv[u] = __ldcg(wp[u]);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kRowUnroll; ++u) {
-            if (wp[u]) {
-                wv[u].x = fma(dd[u], tv[u].x, wv[u].x);
-                wv[u].y = fma(dd[u], tv[u].y, wv[u].y);
-                *wp[u] = wv[u];
-            }
-        }
-    }
-}
-
-// Same row streams, with the loads moved off the register file: every apply
-// thread keeps kAsyncStages items in flight through its own ring of
+// Row streams of delta-list entries [e_lo, e_hi) (shared-memory indices; only batch phase
+// `only` when only >= 0): W[dst, own] = fma(d, T[src, own], W[dst, own]) for both rows of every
+// pair, with the loads off the register file: every apply
+// thread keeps S items in flight through its own ring of
 // shared-memory slots (cp.async, 32 B per item: the W and T chunk), so an SM
-// holds kApply * kAsyncStages * 32 B of row traffic in flight instead of the
-// 2 * kRowUnroll double2 pairs the registers allow. Each thread only reads the
+// holds kApply * S * 32 B of row traffic in flight instead of the few double2 pairs the
+// registers allow. Each thread only reads the
 // slots it filled, so no barrier is needed; cp.async.wait_group orders them.
-// The item -> (entry, half, chunk) mapping and the FMA are those of apply_rows.
 __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double* L_d, const int* L_ph, int only,
                                                  int e_lo, int e_hi, int w2, double* __restrict__ Wb,
                                                  const double* __restrict__ Tb, double2* ring, int ta, int S) {
@@ -1029,7 +981,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             }
             idle_since = 0;
 
-#if QB_ASYNC_HEADS
             // ---- segment heads (count + first entry) of the batch's colours: copied
             // asynchronously into shared memory while this thread stages (below); every
             // thread then reads back only the heads it copied
@@ -1050,30 +1001,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                              : "memory");
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
-#else
-            // ---- segment heads (count + first entry) of the batch's colours
-            for (int idx = ta; idx < nseg; idx += kApply) {
-                const int jb = idx / nsh;
-                const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
-                const int cnt = __ldcg(lcntL + seg);
-                const int2 rs = __ldcg(lrsL + (size_t)seg * a.share);
-                const double2 dn = __ldcg(ldnL + (size_t)seg * a.share);
-                sm.s_off()[idx] = cnt;
-                if (cnt > 1) s_multi = 1;
-                if (cnt == 1) {
-                    const int pos = atomicAdd(&s_nent, 1);
-                    if (pos < kPairCap) {
-                        sm.L_rs()[pos] = rs;
-                        sm.L_d()[pos] = dn.x;
-                        sm.L_ph()[pos] = jb;
-                    } else {
-                        s_multi = 1;
-                    }
-                    if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
-                    if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
-                }
-            }
-#endif
             // ---- stage block sb: cells brought forward from this slab's watermark C to C'
             if (can_stage) {
                 const long long ts = PCLK();
@@ -1143,7 +1070,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 }
                 t_stage += PCLK() - ts;
             }
-#if QB_ASYNC_HEADS
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             for (int idx = ta; idx < nseg; idx += kApply) {
                 const int jb = idx / nsh;
@@ -1164,7 +1090,6 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
                 }
             }
-#endif
             bar_apply();
             const long long th1 = PCLK();
             if (can_stage) {

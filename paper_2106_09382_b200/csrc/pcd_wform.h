@@ -92,9 +92,6 @@ struct WformArgs {
 #ifndef QB_CHAIN_WARPS
 #define QB_CHAIN_WARPS 6     // chain warps of the blocked kernel (the block's cells are loaded in parallel)
 #endif
-#ifndef QB_ASYNC_HEADS
-#define QB_ASYNC_HEADS 1     // blocked kernel: segment heads copied asynchronously while the apply warps stage
-#endif
 #define WFORM_CHAIN_WARPS_QB QB_CHAIN_WARPS
 #ifndef QB_DEFAULT_D
 #define QB_DEFAULT_D 4
