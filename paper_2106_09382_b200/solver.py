@@ -5,7 +5,10 @@ arguments, return type and exceptions of the reference driver
 (/root/reference/pkg/src/parconcord/solver.py:254-294).  With the default
 backend ("cuda") the whole fit -- every colour of every sweep, the diagonal
 step, the max |delta| convergence test and the objective trace -- runs in ONE
-persistent cooperative kernel on a device-resident W = Omega*T (pcd_wform.cu).
+persistent cooperative kernel on a device-resident W = Omega*T (pcd_qblock.cu,
+D colours per grid barrier; pcd_wform.cu for p < 256 and multi-GPU shards).
+`pcd_path(..., concurrency=k)` runs a cold lambda path on k lanes of SMs
+(`PathScheduler`).
 
 backend="cuda-exact" instead runs the reference's own driver loop over GPU
 sweeps that reproduce the compiled reference kernel bit for bit
