@@ -1,12 +1,18 @@
 #!/bin/bash
-# One gpurun call collecting the round's evidence (bench line, ncu launch list, lambda-path
-# DRAM traffic, one full ncu capture of the fit kernel, phase profiles, racecheck).
+# One gpurun call collecting the round's evidence (bench line, reference arm, ncu launch list,
+# lambda-path DRAM traffic, one full ncu capture of the fit kernel, phase profiles).
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/status.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/status.txt
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1
 echo "bench rc=$?" >> gpurun_out/status.txt
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_launch.log 2>&1
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1
+echo "bench ref rc=$?" >> gpurun_out/status.txt
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/status.txt
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:pcd_ --csv \
     --log-file gpurun_out/traffic.csv python tools/ncu_fits.py > gpurun_out/ncu_traffic.log 2>&1
@@ -14,9 +20,6 @@ echo "ncu traffic rc=$?" >> gpurun_out/status.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:pcd_qblock -c 1 -o gpurun_out/prof_qblock \
     python tools/profile_fit.py --p 5000 --n 2000 --lam 0.3 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/status.txt
-for lam in 0.3 0.15 0.1; do
+for lam in 0.3 0.1; do
   CONCORD_PHASE_PROFILE=1 timeout 300 python tools/profile_fit.py --p 5000 --n 2000 --lam $lam > gpurun_out/phase_l$lam.log 2>&1
 done
-timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard python tools/profile_fit.py --p 300 --n 200 --lam 0.1 \
-    > gpurun_out/racecheck.log 2>&1
-echo "racecheck rc=$?" >> gpurun_out/status.txt
