@@ -358,12 +358,12 @@ def test_result_arrays_are_independent_pinned_pool(golden):
         assert_close_support(r4.estimate.omega, c["omega"])
 
 
-@pytest.mark.parametrize("k", [2, 3])
-def test_concurrent_lambda_path_equals_sequential_fits(k):
+@pytest.mark.parametrize("k,p", [(2, 1000), (3, 1000), (3, 777), (3, 300)])
+def test_concurrent_lambda_path_equals_sequential_fits(k, p):
     """pcd_path(concurrency=k) (PathScheduler): k cold fits at a time on SMs/k slabs each, own
     stream and thread, while sparse, then one at a time on all SMs -- the same bits and iteration
     counts as one fit at a time on all SMs."""
-    _, t = synth.problem("ar2", 1000, 400, seed=7)
+    _, t = synth.problem("ar2", p, 400, seed=7)
     g = cb.GramMatrix(t, 400)
     lams = [0.4, 0.3, 0.2, 0.15, 0.1]
     seq = cb.pcd_path(g, lams, max_outer_iterations=300)
