@@ -188,21 +188,33 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
     const int per = 2 * w2;
     const int items = (e_hi - e_lo) * per;
     const int nmine = items > ta ? (items - ta + kApply - 1) / kApply : 0;
-    auto locate = [&](int i, int& e, int& off_w, int& off_t) {
-        const int idx = ta + i * kApply;
-        const int q = idx / per;
-        e = e_lo + q;
-        const int rem = idx - q * per;
-        const int h = rem >= w2;
-        const int j2 = rem - h * w2;
+    // item idx = ta + i * kApply -> (entry q, position rem in the entry), stepped without division
+    const int dq = kApply / per, dr = kApply - dq * per;
+    struct Cursor {
+        int q, rem;
+    };
+    auto step = [&](Cursor& c) {
+        c.q += dq;
+        c.rem += dr;
+        if (c.rem >= per) {
+            c.rem -= per;
+            ++c.q;
+        }
+    };
+    auto locate = [&](const Cursor& c, int& e, int& off_w, int& off_t) {
+        e = e_lo + c.q;
+        const int h = c.rem >= w2;
+        const int j2 = c.rem - h * w2;
         const int2 rs = L_rs[e];
         off_w = (h ? rs.y : rs.x) * w2 + j2;
         off_t = (h ? rs.x : rs.y) * w2 + j2;
     };
+    Cursor ci{ta / per, ta - (ta / per) * per};  // next item to issue
+    Cursor cc = ci;                               // next item to complete
     int si = 0, sc = 0;  // ring slots of the next issue / the next completion
-    auto issue = [&](int i) {
+    auto issue = [&]() {
         int e, ow, ot;
-        locate(i, e, ow, ot);
+        locate(ci, e, ow, ot);
         if (only < 0 || L_ph[e] == only) {
             double2* slot = ring + (size_t)(si * 2) * kApply + ta;
             const unsigned sw = (unsigned)__cvta_generic_to_shared(slot);
@@ -216,14 +228,16 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         si = (si + 1 == S) ? 0 : si + 1;
+        step(ci);
     };
     // prologue: S - 1 items in flight; then one issue per completed item, and in the
     // tail (nothing left to issue) wait for everything.  S is 2, 4, 6 or 8 (shared-memory budget).
     int ni = min(nmine, S - 1);
-    for (int i = 0; i < ni; ++i) issue(i);
+    for (int i = 0; i < ni; ++i) issue();
     for (int j = 0; j < nmine; ++j) {
         if (ni < nmine) {
-            issue(ni++);
+            issue();
+            ++ni;
             if (S == 8) asm volatile("cp.async.wait_group 7;" ::: "memory");
             else if (S == 6) asm volatile("cp.async.wait_group 5;" ::: "memory");
             else if (S == 4) asm volatile("cp.async.wait_group 3;" ::: "memory");
@@ -232,7 +246,7 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         int e, ow, ot;
-        locate(j, e, ow, ot);
+        locate(cc, e, ow, ot);
         if (only < 0 || L_ph[e] == only) {
             const double2* slot = ring + (size_t)(sc * 2) * kApply + ta;
             double2 wv = slot[0];
@@ -243,6 +257,7 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
             reinterpret_cast<double2*>(Wb)[ow] = wv;
         }
         sc = (sc + 1 == S) ? 0 : sc + 1;
+        step(cc);
     }
 }
 
@@ -328,6 +343,7 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsi
     int spins = 0;
     do {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (v < target) __nanosleep(20);  // leave the issue slots to the apply warps of this SMSP
         if (++spins == 4096) {
             spins = 0;
             if (globaltimer_ns() - t0 > kHangNs) hang_report(hang, 0, blk, (long long)v, (long long)target, 0, 0);
@@ -888,6 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const long long tw0 = PCLK();
                     const unsigned long long g0t = globaltimer_ns();
                     while (ld_acquire_cta(&s_staged) < blk + 2) {
+                        __nanosleep(20);
                         if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, blk, blk + 2, ld_vol(&s_staged), 0, 0);
                     }
                     t_c3 += PCLK() - tw0;
