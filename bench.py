@@ -8,8 +8,8 @@ p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
 the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = the whole path:
 ten complete cold-start CONCORD-PCD fits (identity init, delta_tol 1e-5),
 scheduled by the package's PathScheduler -- --concurrency k (default 3)
-lanes, each a solver on its own share of the SMs (k=3: 74/37/37; own stream
-and host thread), pull the fits densest first (one latency-bound fit leaves
+lanes, each a solver on its own share of the SMs (k=3: 66/41/41 on a B200; own
+stream and host thread), pull the fits densest first (one latency-bound fit leaves
 most of a B200 idle; longest job first balances the lanes).  --concurrency 1 runs every
 fit on all SMs, one after the other.
 The metric is sweeps/s (outer iterations per second, BASELINE "sweeps/sec"),

@@ -321,9 +321,8 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
     (a non-converged fit is returned with converged=False, not raised).
 
     concurrency=k (cold mode) runs the fits on k lanes, each a solver on its
-    own share of the SMs (k=3: half the device, then two quarters), densest
-    lambda first (`PathScheduler`); the results are bitwise those of
-    sequential fits.
+    own share of the SMs (k=3 on a B200: 66/41/41), densest lambda first
+    (`PathScheduler`); the results are bitwise those of sequential fits.
     """
     if concurrency > 1:
         if warm_start:
@@ -347,7 +346,7 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
 
 class PathScheduler:
     """Cold lambda path on one device: k lanes, each a solver on its own share of the SMs
-    (k=3: half the device, then two quarters).
+    (k=3 on a B200: 66/41/41 SMs).
 
     A sparse fit is latency-bound: one fit leaves most of a B200 idle, and two fits on halves of
     the device (own solver, stream and host thread) finish ~1.6x sooner than one after the other
@@ -363,16 +362,17 @@ class PathScheduler:
         e.g. (74, 37, 37) -- the densest fit on the largest lane, the sparse ones on the others."""
         nsm = _lib.device_sm_count(device)
         if lanes is None:
-            # one lane of half the device for the densest fits, the other half split evenly: the
-            # sparse fits are latency-bound, so smaller lanes lose little per fit and add lanes
-            # (p=5000 path: 74/74 -> 3.15 s, 74/37/37 -> 2.78 s, 74/25/25/24 -> 3.08 s)
+            # one large lane (9/20 of the device) for the densest fits, the rest split evenly:
+            # the sparse fits are latency-bound, so smaller lanes lose little per fit and add
+            # lanes (p=5000 path on 148 SMs: 74/74 -> 3.15 s, 74/37/37 -> 2.67 s, 66/41/41 ->
+            # 2.55 s, 60/30/30/28 -> 2.62 s; profiles/r01/v6/lane_split_sweep.log)
             if k <= 1:
                 lanes = []
             elif k == 2:
                 lanes = [nsm // 2, nsm // 2]
             else:
-                rest = nsm - nsm // 2
-                lanes = [nsm // 2] + [rest // (k - 1)] * (k - 1)
+                big = nsm * 9 // 20
+                lanes = [big] + [(nsm - big) // (k - 1)] * (k - 1)
         lanes = sorted((int(v) for v in lanes), reverse=True)
         if sum(lanes) > nsm or any(v < 1 for v in lanes):
             raise ValueError(f"lanes {lanes} do not fit the device's {nsm} SMs")
