@@ -133,6 +133,9 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
     const int w = 2 * w2;
     const int per = 2 * w2;
     const int items = (e_hi - e_lo) * per;
+    // item idx = ta + (k * kRowUnroll + u) * kApply -> (entry q, position rem), stepped without division
+    const int dq = kApply / per, dr = kApply - dq * per;
+    int q = ta / per, rem = ta - (ta / per) * per;
     for (int base = 0; base < items; base += kApply * kRowUnroll) {
         double2 tv[kRowUnroll], wv[kRowUnroll];
         double2* wp[kRowUnroll];
@@ -142,9 +145,8 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
             const int idx = base + u * kApply + ta;
             wp[u] = nullptr;
             if (idx < items) {
-                const int e = e_lo + idx / per;
+                const int e = e_lo + q;
                 if (only < 0 || L_ph[e] == only) {
-                    const int rem = idx - (idx / per) * per;
                     const int h = rem >= w2;
                     const int j2 = rem - h * w2;
                     const int2 rs = L_rs[e];
@@ -155,6 +157,12 @@ __device__ __forceinline__ void apply_rows(const int2* L_rs, const double* L_d, 
                     tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + (long long)src * w) + j2);
                     wv[u] = __ldcg(wp[u]);
                 }
+            }
+            q += dq;
+            rem += dr;
+            if (rem >= per) {
+                rem -= per;
+                ++q;
             }
         }
 #pragma unroll
@@ -395,6 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                 if (tc < wl) {
                     const unsigned long long g0t = globaltimer_ns();
                     while (ld_acquire_cta(&s_staged) < Q) {
+                        __nanosleep(20);
                         if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, g, Q, ld_vol(&s_staged), 0, 0);
                     }
                 }
