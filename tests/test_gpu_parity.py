@@ -375,3 +375,16 @@ def test_concurrent_lambda_path_equals_sequential_fits(k, p):
         np.testing.assert_allclose(a.objective_trace, b.objective_trace, rtol=1e-12)
     with pytest.raises(ValueError):
         cb.pcd_path(g, lams, warm_start=True, concurrency=k)
+
+
+def test_concurrent_lambda_path_from_data_matrix():
+    """pcd_path(DataMatrix, concurrency=3) computes the Gram on the device first; same bits as
+    sequential fits from the same data."""
+    x, _ = synth.problem("ar2", 600, 300, seed=11)
+    dm = cb.DataMatrix(x, centered=True)
+    lams = [0.3, 0.15]
+    seq = cb.pcd_path(dm, lams, max_outer_iterations=300)
+    con = cb.pcd_path(dm, lams, max_outer_iterations=300, concurrency=3)
+    for a, b in zip(seq, con):
+        assert a.iterations == b.iterations
+        assert np.array_equal(a.estimate.omega, b.estimate.omega)
