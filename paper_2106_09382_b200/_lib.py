@@ -221,16 +221,19 @@ class _PooledOwner:
 
     def __del__(self):
         try:
-            free = _POOL.setdefault(self.nbytes, [])
-            if (len(free) + 1) * self.nbytes <= _POOL_KEEP_BYTES or not free:
-                free.append(self.addr)
-            else:
+            with _POOL_LOCK:
+                free = _POOL.setdefault(self.nbytes, [])
+                keep = (len(free) + 1) * self.nbytes <= _POOL_KEEP_BYTES or not free
+                if keep:
+                    free.append(self.addr)
+            if not keep:
                 load().concord_host_free(ctypes.c_void_p(self.addr))
         except Exception:
             pass
 
 
 _POOL = {}  # nbytes -> free page-locked blocks
+_POOL_LOCK = threading.Lock()  # lanes of a PathScheduler take and return blocks concurrently
 _POOL_KEEP_BYTES = 4 << 30  # per block size (a lambda path keeps ten 200 MB results alive at p=5000)
 
 
@@ -262,10 +265,10 @@ def pooled_pinned_empty(shape, dtype=None):
     nbytes = max(count * dtype.itemsize, 1)
     if device_count() < 1:
         return np.empty(shape, dtype)
-    free = _POOL.get(nbytes)
-    if free:
-        addr = free.pop()
-    else:
+    with _POOL_LOCK:
+        free = _POOL.get(nbytes)
+        addr = free.pop() if free else None
+    if addr is None:
         raw = ctypes.c_void_p()
         check(load().concord_host_alloc(nbytes, ctypes.byref(raw)))
         addr = raw.value

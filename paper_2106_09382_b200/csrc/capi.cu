@@ -140,7 +140,7 @@ struct concord_solver {
     long long* rec_nnz = nullptr;
     int rec_cap = 0;
     int last_iters = 0;
-    int* csr_rowptr = nullptr;
+    long long* csr_rowptr = nullptr;  // int64: a dense init at p >= 46341 has > 2^31 entries
     int* csr_col = nullptr;
     double* csr_val = nullptr;
     long long csr_cap = 0;
@@ -230,7 +230,8 @@ int init_warm(concord_solver* s, const double* om, int32_t where) {
         CK(cudaStreamSynchronize(s->stream));
         h = host.data();
     }
-    std::vector<int> rowptr(p + 1, 0), col;
+    std::vector<long long> rowptr(p + 1, 0);
+    std::vector<int> col;
     std::vector<double> val;
     for (int i = 0; i < p; ++i) {
         const double* row = h + (size_t)i * p;
@@ -239,7 +240,7 @@ int init_warm(concord_solver* s, const double* om, int32_t where) {
                 col.push_back(j);
                 val.push_back(row[j]);
             }
-        rowptr[i + 1] = (int)col.size();
+        rowptr[i + 1] = (long long)col.size();
     }
     const long long nnz = (long long)col.size();
     if (nnz > s->csr_cap) {
@@ -252,7 +253,7 @@ int init_warm(concord_solver* s, const double* om, int32_t where) {
         s->csr_cap = nnz;
     }
     if (!s->csr_rowptr) CK(dalloc(&s->csr_rowptr, p + 1));
-    CK(cudaMemcpyAsync(s->csr_rowptr, rowptr.data(), sizeof(int) * (p + 1), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->csr_rowptr, rowptr.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s->stream));
     if (nnz) {
         CK(cudaMemcpyAsync(s->csr_col, col.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, s->stream));
         CK(cudaMemcpyAsync(s->csr_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s->stream));

@@ -144,6 +144,12 @@ __device__ __forceinline__ void hang_report(long long* hang, int what, int blk, 
 }
 
 
+// |delta| for the convergence max, with NaN mapped to +inf: fmax / warp_max drop a NaN
+// operand, and the reference's np.max(np.abs(...)) (solver.py:141-163) never converges on one.
+__device__ __forceinline__ double abs_delta(double d) {
+    return (d != d) ? __longlong_as_double(0x7ff0000000000000ll) : fabs(d);
+}
+
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 
 template <typename T>

@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             a.dring[dgo + r] = dl;  // 0 when the partner is the phantom (odd p)
                             if (s < p) a.dring[dgo + s] = dl;
                             if (dl != 0.0) {
-                                smax = fmax(smax, fabs(dl));
+                                smax = fmax(smax, abs_delta(dl));
                                 ++snnz;
                             }
                         }
@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         const double dl = __dsub_rn(nv, om);
                         a.dring[dgo + x] = dl;
                         a.diagv[x] = make_double2(dl, nv);
-                        dm = fmax(dm, fabs(dl));
+                        dm = fmax(dm, abs_delta(dl));
                     }
                     // this sweep's statistics: off-diagonal (own pairs) and diagonal maxima, non-zero count
                     const double mw = warp_max(fmax(dm, smax));

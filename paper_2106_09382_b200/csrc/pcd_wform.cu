@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                     dd[i] = make_double2(d, nv);
                     if ((unsigned)(i - c0) < (unsigned)wl)
                         FOR_COPIES(r) a.x.dring[r][dg_off + i] = d;
-                    dm = fmax(dm, fabs(d));
+                    dm = fmax(dm, abs_delta(d));
                 }
                 dm = warp_max(dm);
                 if (lane == 0) s_red[0][warp] = dm;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
                                 a.x.dring[c][dg_off + s] = d;
                             }
                             if (d != 0.0) {
-                                smax = fmax(smax, fabs(d));
+                                smax = fmax(smax, abs_delta(d));
                                 ++snnz;
                             }
                         } else {
@@ -956,7 +956,7 @@ __global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, i
 
 // W (slab) = Omega_init * T for a warm start, from a CSR copy of Omega_init.
 // Row i of W is sum_k om[i,k] T[k,:]; each block streams its own slab.
-__global__ void wform_init_csr_kernel(const int* __restrict__ rowptr, const int* __restrict__ colidx,
+__global__ void wform_init_csr_kernel(const long long* __restrict__ rowptr, const int* __restrict__ colidx,
                                       const double* __restrict__ vals, const double* __restrict__ Tslab,
                                       double* __restrict__ Wslab, int p, int w) {
     const int b = blockIdx.y;
@@ -969,7 +969,7 @@ __global__ void wform_init_csr_kernel(const int* __restrict__ rowptr, const int*
         const int i = (int)(idx / w2);
         const int j2 = (int)(idx - (long long)i * w2);
         double2 acc = make_double2(0.0, 0.0);
-        for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+        for (long long e = rowptr[i]; e < rowptr[i + 1]; ++e) {
             const double v = vals[e];
             const double2 tv = __ldg(reinterpret_cast<const double2*>(Tb + (long long)colidx[e] * w) + j2);
             acc.x = fma(v, tv.x, acc.x);
@@ -1070,7 +1070,7 @@ cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_wform_init_csr(const int* rowptr, const int* colidx, const double* vals, const double* Tslab,
+cudaError_t launch_wform_init_csr(const long long* rowptr, const int* colidx, const double* vals, const double* Tslab,
                                   double* Wslab, int p, int w, int nblk, cudaStream_t st) {
     long long items = (long long)p * (w >> 1);
     int gx = (int)((items + 255) / 256);

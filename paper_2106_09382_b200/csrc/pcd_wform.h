@@ -158,7 +158,7 @@ cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, in
 cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, int blk0, cudaStream_t st);
 cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, int blk0, unsigned long long* out,
                                    cudaStream_t st);
-cudaError_t launch_wform_init_csr(const int* rowptr, const int* colidx, const double* vals, const double* Tslab,
+cudaError_t launch_wform_init_csr(const long long* rowptr, const int* colidx, const double* vals, const double* Tslab,
                                   double* Wslab, int p, int w, int nblk, cudaStream_t st);
 // Diagonal of a row-major p x p matrix (the replicated T diagonal).
 cudaError_t launch_rowmajor_diag(const double* src, double* diag, int p, cudaStream_t st);

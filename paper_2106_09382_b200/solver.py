@@ -16,9 +16,11 @@ sweeps that reproduce the compiled reference kernel bit for bit
 backend: without the CUDA library or a device every entry point raises.
 """
 
+import contextlib
 import ctypes
 import math
 import os
+import threading
 import time
 from dataclasses import dataclass
 
@@ -297,8 +299,12 @@ class Solver:
     def fit(self, lam, delta_tol=1e-5, max_iter=200, init=None, trace=True, raise_on_cap=True) -> FitReport:
         rc, res, deltas, objs, secs = self.fit_raw(lam, delta_tol, max_iter, init, trace)
         om = self.omega()
+        # A converged fit's estimate is exactly symmetric with a positive diagonal by construction
+        # (both mirrored cells get the same value; the diagonal closed form is positive).  A fit
+        # that hit the cap may have diverged (non-finite data): validate it the way the
+        # reference's _finish does (solver.py:214-224 -> model.py:117-120), which raises.
         report = FitReport(
-            estimate=PrecisionEstimate._trusted(om),
+            estimate=PrecisionEstimate._trusted(om) if res.converged else PrecisionEstimate(om),
             iterations=int(res.iterations),
             final_delta=float(res.final_delta),
             converged=bool(res.converged),
@@ -328,19 +334,20 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
         if warm_start:
             raise ValueError("warm starts chain the fits: concurrency must be 1")
         return _path_concurrent(x_or_gram, lams, delta_tol, max_outer_iterations, device, trace, int(concurrency))
-    s = _pooled_solver(_gram_p(x_or_gram), device)  # T resident for the whole path
-    if isinstance(x_or_gram, DataMatrix):
-        s.gram_from_data(x_or_gram)
-    elif isinstance(x_or_gram, GramMatrix):
-        s.set_gram(x_or_gram)
-    else:
-        raise TypeError("expected a DataMatrix or GramMatrix")
-    reports, prev = [], None
-    for lam in lams:
-        rep = s.fit(lam, delta_tol, max_outer_iterations, init=prev if warm_start else None, trace=trace,
-                    raise_on_cap=False)
-        reports.append(rep)
-        prev = rep.estimate.omega
+    with _checkout((_gram_p(x_or_gram), int(device)), lambda: Solver(_gram_p(x_or_gram), device=device)) as s:
+        # T resident for the whole path
+        if isinstance(x_or_gram, DataMatrix):
+            s.gram_from_data(x_or_gram)
+        elif isinstance(x_or_gram, GramMatrix):
+            s.set_gram(x_or_gram)
+        else:
+            raise TypeError("expected a DataMatrix or GramMatrix")
+        reports, prev = [], None
+        for lam in lams:
+            rep = s.fit(lam, delta_tol, max_outer_iterations, init=prev if warm_start else None, trace=trace,
+                        raise_on_cap=False)
+            reports.append(rep)
+            prev = rep.estimate.omega
     return reports
 
 
@@ -458,15 +465,10 @@ def _path_concurrent(x_or_gram, lams, delta_tol, max_outer_iterations, device, t
     else:
         raise TypeError("expected a DataMatrix or GramMatrix")
     key = ("path", gram.p, int(device), int(k))
-    sched = _POOL.get(key)
-    if sched is None or any(s._h is None for s in sched.solvers):
-        if len(_POOL) >= 2:
-            release_device_memory()
-        sched = PathScheduler(gram.p, device=device, k=k)
-        _POOL[key] = sched
-    sched.set_gram(gram)
-    return sched.run(lams, lambda s, lam: s.fit(lam, delta_tol, max_outer_iterations, trace=trace,
-                                                raise_on_cap=False))
+    with _checkout(key, lambda: PathScheduler(gram.p, device=device, k=k)) as sched:
+        sched.set_gram(gram)
+        return sched.run(lams, lambda s, lam: s.fit(lam, delta_tol, max_outer_iterations, trace=trace,
+                                                    raise_on_cap=False))
 
 
 def _gram_p(x):
@@ -475,27 +477,55 @@ def _gram_p(x):
     raise TypeError("expected a DataMatrix or GramMatrix")
 
 
-# Device buffers are reused across pcd_fit calls of the same size and device
-# (allocation of 4 x 8p^2 bytes per call would otherwise dominate small fits).
-_POOL = {}
+# Device solvers are reused across pcd_fit / pcd_path calls of the same size and device
+# (allocating 3 x 8p^2 bytes per call would otherwise dominate small fits).  A call checks
+# one out EXCLUSIVELY: concurrent callers of the same p get solvers of their own, so pcd_fit
+# stays re-entrant like the reference's pure function (solver.py:254-294), and
+# release_device_memory() never closes a solver in use (it is closed when returned).
+_POOL_LOCK = threading.Lock()
+_POOL = {}  # key -> idle Solver / PathScheduler objects
+_POOL_KEYS = 2  # problem sizes kept resident
+_POOL_GEN = [0]  # bumped by release_device_memory()
 
 
-def _pooled_solver(p, device):
-    key = (int(p), int(device))
-    s = _POOL.get(key)
-    if s is None or s._h is None:
-        if len(_POOL) >= 2:
-            release_device_memory()
-        s = Solver(p, device=device)
-        _POOL[key] = s
-    return s
+def _alive(obj):
+    return all(s._h is not None for s in (obj.solvers if isinstance(obj, PathScheduler) else [obj]))
+
+
+@contextlib.contextmanager
+def _checkout(key, make):
+    evict = []
+    with _POOL_LOCK:
+        idle = _POOL.get(key)
+        obj = idle.pop() if idle else None
+        if obj is None and key not in _POOL and len(_POOL) >= _POOL_KEYS:
+            evict = [o for k in list(_POOL) for o in _POOL.pop(k)]  # free device memory for a new size
+        gen = _POOL_GEN[0]
+    for o in evict:
+        o.close()
+    if obj is not None and not _alive(obj):
+        obj = None
+    if obj is None:
+        obj = make()
+    try:
+        yield obj
+    finally:
+        with _POOL_LOCK:
+            keep = gen == _POOL_GEN[0] and _alive(obj)
+            if keep:
+                _POOL.setdefault(key, []).append(obj)
+        if not keep:
+            obj.close()
 
 
 def release_device_memory():
-    """Free the device buffers pcd_fit keeps for reuse."""
-    for v in list(_POOL.values()):
-        v.close()
-    _POOL.clear()
+    """Free the device buffers pcd_fit keeps for reuse (solvers in use are freed when returned)."""
+    with _POOL_LOCK:
+        _POOL_GEN[0] += 1
+        objs = [o for v in _POOL.values() for o in v]
+        _POOL.clear()
+    for o in objs:
+        o.close()
 
 
 # --------------------------------------------------------------- the drivers
@@ -531,10 +561,10 @@ def pcd_fit(x_or_gram, config: SolverConfig, schedule: Schedule = None, backend=
     if init is not None and init.p != p:
         raise DimensionError(f"init has p={init.p} but the problem has p={p}")
     if name == "cuda" and custom is None:
-        s = _pooled_solver(p, device)
-        s.set_gram(gram)
-        return s.fit(config.lam, config.delta_tol, config.max_outer_iterations,
-                     init=None if init is None else init.omega, trace=True)
+        with _checkout((p, int(device)), lambda: Solver(p, device=device)) as s:
+            s.set_gram(gram)
+            return s.fit(config.lam, config.delta_tol, config.max_outer_iterations,
+                         init=None if init is None else init.omega, trace=True)
     # Reference driver loop over the bit-exact GPU sweeps (also any non-circle schedule).
     from . import cuda_kernels
 

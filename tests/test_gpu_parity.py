@@ -7,6 +7,8 @@ in FP64", identical sparsity and schedule):
     identical support, edge count and iteration count; objective trace rtol 1e-10.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -92,14 +94,47 @@ def test_wform_fit_matches_reference(golden, name):
     assert all(t > 0 for t in rep.wall_time_per_iteration)
 
 
-@pytest.mark.parametrize("kind,p", [("scale_free", 1000), ("scale_free", 1001), ("ar2", 1000)])
-def test_wform_config2_matches_oracle(oracle, kind, p):
-    _, t = synth.problem(kind, p, 500, seed=0)
-    ref = oracle.pcd_fit(t, 500, 0.3, 1e-5, 5000, workers=8, trace=False)
-    rep = cb.pcd_fit(cb.GramMatrix(t, 500), cb.SolverConfig(lam=0.3, max_outer_iterations=5000))
+CONFIG2 = [("scale_free", 1000, 500, 0.3), ("scale_free", 1001, 500, 0.3), ("ar2", 1000, 500, 0.3),
+           # dense regime: 5-12% of the pairs move per sweep, so the blocked kernel's conflict paths
+           # (per-row chains, phase-by-phase passes, multi-entry segments) carry the fit
+           ("scale_free", 1000, 500, 0.1), ("scale_free", 1001, 500, 0.1), ("ar2", 1000, 500, 0.1),
+           ("ar2", 2001, 1000, 0.1)]
+
+
+@pytest.mark.parametrize("kind,p,n,lam", CONFIG2)
+def test_wform_config2_matches_oracle(oracle, kind, p, n, lam):
+    """BASELINE configs[1] (p=1000 / odd 1001, n=500) at lam 0.3 and 0.1, and p=2001 dense: the
+    fast fit against the oracle (bitwise the compiled reference) on the same T."""
+    _, t = synth.problem(kind, p, n, seed=0)
+    ref = oracle.pcd_fit(t, n, lam, 1e-5, 5000, workers=os.cpu_count(), trace=True)
+    rep = cb.pcd_fit(cb.GramMatrix(t, n), cb.SolverConfig(lam=lam, max_outer_iterations=5000))
     assert rep.iterations == ref["iterations"]
     assert rep.edge_count == ref["edge_count"]
     assert_close_support(rep.estimate.omega, ref["omega"])
+    np.testing.assert_allclose(rep.objective_trace, ref["objective_trace"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("row", range(3))
+def test_config2_reference_summaries(golden, row):
+    """`big_summary` recorded from the REAL reference package (make_golden.py): iterations, edges,
+    final delta and last objective of the fast fit; the exact backend reproduces the reference's
+    Omega bitwise (sha256 `big_*_omsha`)."""
+    import hashlib
+
+    kind_id, p, n, lam, iters, edges, delta, obj = golden["big_summary"][row]
+    kind = "ar2" if kind_id == 0 else "scale_free"
+    p, n = int(p), int(n)
+    _, t = synth.problem(kind, p, n, seed=0)
+    assert hashlib.sha256(t.tobytes()).hexdigest() == bytes(golden[f"big_{kind}_{p}_tsha"]).decode()
+    g = cb.GramMatrix(t, n)
+    cfg = cb.SolverConfig(lam=lam, max_outer_iterations=5000)
+    rep = cb.pcd_fit(g, cfg)
+    assert rep.iterations == int(iters) and rep.edge_count == int(edges)
+    assert rep.final_delta == pytest.approx(delta, rel=1e-6)
+    assert rep.objective_trace[-1] == pytest.approx(obj, rel=1e-10)
+    ex = cb.pcd_fit(g, cfg, backend="cuda-exact")
+    assert ex.iterations == int(iters) and ex.final_delta == delta
+    assert hashlib.sha256(ex.estimate.omega.tobytes()).hexdigest() == bytes(golden[f"big_{kind}_{p}_omsha"]).decode()
 
 
 @pytest.mark.parametrize("p,lam", [(2, 0.1), (3, 0.05), (5, 0.0), (64, 0.0), (257, 0.2)])

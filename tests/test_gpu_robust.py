@@ -1,0 +1,85 @@
+"""GPU robustness: diverging fits and concurrent callers.
+
+* A fit whose iterate goes non-finite (an infinite Gram entry, or a non-PSD Gram
+  with lam=0) must never report convergence.  The reference's delta
+  np.max(np.abs(...)) propagates NaN, so it runs to the cap and its _finish
+  validation raises ValueError ("estimate must be exactly symmetric";
+  /root/reference/pkg/src/parconcord/solver.py:214-224, model.py:117-120).
+  The device max maps a NaN delta to +inf (common.cuh abs_delta) and the host
+  validates every estimate of a fit that hit the cap, so the same ValueError
+  comes out of both kernels (per-phase p < 256, blocked p >= 256) and the
+  exact backend.
+* pcd_fit is re-entrant like the reference's pure function: threads fitting
+  the same p check out solvers of their own from the pool.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2106_09382_b200 as cb
+from paper_2106_09382_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _gram(p, case):
+    rng = np.random.default_rng(p)
+    x = rng.standard_normal((4 * p, p))
+    t = synth.host_gram(x)
+    if case == "inf":
+        t[0, 1] = t[1, 0] = np.inf
+        lam = 0.1
+    else:  # symmetric, positive diagonal, not positive semi-definite
+        t[0, 1] = t[1, 0] = 1e3 * t[0, 0]
+        lam = 0.0
+    return cb.GramMatrix(t, 4 * p), lam
+
+
+@pytest.mark.parametrize("p", [10, 300])
+@pytest.mark.parametrize("case", ["inf", "nonpsd"])
+@pytest.mark.parametrize("backend", ["cuda", "cuda-exact"])
+def test_non_finite_fit_raises_like_reference(p, case, backend):
+    if backend == "cuda-exact" and p > 10:
+        pytest.skip("exact sweeps are the small-p parity hook")
+    g, lam = _gram(p, case)
+    with pytest.raises(ValueError, match="symmetric|diagonal"):
+        cb.pcd_fit(g, cb.SolverConfig(lam=lam, max_outer_iterations=50), backend=backend)
+
+
+@pytest.mark.parametrize("p", [10, 300])
+def test_diverging_fit_never_reports_convergence(p):
+    g, lam = _gram(p, "inf")
+    with cb.Solver(p) as s:
+        s.set_gram(g)
+        rc, res, deltas, objs, secs = s.fit_raw(lam, 1e-5, 20)
+    assert not res.converged
+    assert res.iterations == 20
+    assert not np.isfinite(res.final_delta) or res.final_delta >= 1e-5
+
+
+def test_concurrent_pcd_fit_same_p_is_reentrant():
+    _, t = synth.problem("ar2", 300, 200, seed=3)
+    g = cb.GramMatrix(t, 200)
+    lams = [0.35, 0.3, 0.25, 0.2, 0.3, 0.35]
+    want = {lam: cb.pcd_fit(g, cb.SolverConfig(lam=lam, max_outer_iterations=500)).estimate.omega.copy()
+            for lam in set(lams)}
+    got, errors = [None] * len(lams), []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                got[i] = cb.pcd_fit(g, cb.SolverConfig(lam=lams[i], max_outer_iterations=500)).estimate.omega.copy()
+        except BaseException as e:
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(lams))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[0]
+    for i, lam in enumerate(lams):
+        assert np.array_equal(got[i], want[lam]), lam
+    cb.release_device_memory()

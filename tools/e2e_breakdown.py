@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 import numpy as np
 import paper_2106_09382_b200 as cb
 from paper_2106_09382_b200 import _lib, synth
-from paper_2106_09382_b200.solver import _pooled_solver
+from paper_2106_09382_b200.solver import Solver
 
 p, n = 5000, 2000
 x = synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
@@ -17,7 +17,7 @@ g = cb.GramMatrix(tp, n)
 cfg = cb.SolverConfig(lam=0.3, max_outer_iterations=5000)
 for rep in range(3):
     t0 = time.perf_counter()
-    s = _pooled_solver(p, 0)
+    s = Solver(p, device=0)
     t1 = time.perf_counter()
     s.set_gram(g)
     t2 = time.perf_counter()
