@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
+    ap.add_argument("--cpu-validate", action="store_true",
+                    help="also run one complete reference fit at lambda=0.3 on the host (minutes)")
     a = ap.parse_args()
     if a.p is None:
         a.p = 20000 if a.mode == "sharded" else 5000
@@ -197,11 +199,18 @@ def ncu_traffic(workload):
 
 
 def make_problem(p, n):
+    """Centred AR(2) samples.  p <= 8000: the reference pipeline rounded onto the exact-Gram grid
+    (synth.portable_problem), so T -- device DMMA Gram included -- is bitwise the T of the
+    reference fixtures in tests/golden/p5000/."""
     from paper_2106_09382_b200 import synth
 
     if p > 8000:  # configs[3:]: banded sampler (same distribution, O(p n))
         return synth.center(synth.sample_mvn_ar2_banded(p, n, seed=0))
-    return synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):
+        x = synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
+    return synth.quantize_exact_gram(x)[0]
 
 
 def algorithmic_bytes(p, nnz_per_sweep, want_trace=True):
@@ -216,7 +225,15 @@ def algorithmic_bytes(p, nnz_per_sweep, want_trace=True):
 
 
 def cpu_reference_rate(t, n, lam, target_s, workers):
-    """Sweeps/s of the reference's compiled pcd_sweep on a bounded sample of rounds."""
+    """Sweeps/s of the reference's own per-iteration work on a bounded sample.
+
+    The compiled pcd_sweep (oracle/_ref: the reference's _ckernels.pyx built
+    here) runs a bounded sample of colour rounds -- its cost is data- and
+    lambda-independent (_ckernels.pyx:33-36) -- and the driver's per-iteration
+    work inside the reference's timed region (solver.py:283-288: the snapshot
+    copy and cyclic_max_reduce(_vech(omega - snapshot))) is timed once at the
+    same p.  Per-sweep seconds = sample / fraction of rounds + that overhead.
+    """
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle as orc
 
@@ -242,8 +259,29 @@ def cpu_reference_rate(t, n, lam, target_s, workers):
     dt = run(0, probe)
     rounds = int(max(probe, min(nrounds, target_s / max(dt / probe, 1e-9))))
     el = run(0, rounds)
+    om = np.eye(p)
+    tic = time.perf_counter()
+    snap = om.copy()
+    orc.cyclic_max_reduce(orc.vech(om - snap))
+    overhead = time.perf_counter() - tic
     # each call also runs the p diagonal updates (1/p of a sweep) -- counted as work done
-    return (rounds / nrounds) / el, kind, rounds, el
+    sweep_s = el * nrounds / rounds + overhead
+    return 1.0 / sweep_s, kind, rounds, el, overhead
+
+
+def cpu_full_fit(t, n, lam, workers):
+    """One complete reference fit (the stock solver.py:254-294 loop over oracle/_ref's pcd_sweep with the
+    reference's numpy convergence metric), timed the reference's way: sum of wall_time_per_iteration."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as orc
+
+    tic = time.perf_counter()
+    rep = orc.pcd_fit(t, n, lam, 1e-5, 5000, workers=workers, trace=False, use_ref=orc.load_ref() is not None,
+                      numpy_delta=True)
+    wall = time.perf_counter() - tic
+    return {"lam": lam, "iterations": rep["iterations"], "edges": rep["edge_count"],
+            "sum_wall_time_per_iteration_s": float(sum(rep["wall_time_per_iteration"])), "wall_s_incl_schedule": wall,
+            "per_sweep_s": float(sum(rep["wall_time_per_iteration"])) / rep["iterations"], "workers": workers}
 
 
 # --------------------------------------------------------------- our arm
@@ -271,7 +309,7 @@ def run_ours(args, d):
     lay = s.layout()
     kernel = f"pcd_qblock_kernel (D={lay['kernel']})" if lay["kernel"] else "pcd_wform_kernel"
     g0 = time.perf_counter()
-    s.gram_from_data(cb.DataMatrix(x, centered=True))
+    s.gram_from_data(cb.DataMatrix(x))  # X is centred (then rounded to the exact-Gram grid)
     gram_s = time.perf_counter() - g0
     g = s.gram()
     sched.set_gram(g)  # every lane's solver (the full-device one is created on demand)
@@ -314,14 +352,33 @@ def run_ours(args, d):
     sweeps = d.sum(sum(f[1] for f in fits))
     value = sweeps / (elapsed_ms / 1e3)
 
-    # roofline of the dominant kernel (the fit kernel): algorithmic bytes of all fits over the
-    # device time they took (the concurrent fits' launches overlap, so it is aggregate)
+    # roofline of the dominant kernel (the fit kernel, one persistent launch per fit).  The recipe's
+    # figure: algorithmic bytes per launch / the average launch duration (CUDA events on the launching
+    # stream).  With k lanes the launches overlap on disjoint SM sets, so the device-level HBM
+    # utilisation (all fits' bytes / the steps' device time) is reported beside it, as is every
+    # lambda's own launch (on its lane's SMs) and two fits alone on the full device.
     kern_ms = [f[2] for f in fits]
     bytes_per = [algorithmic_bytes(p, f[3]) for f in fits]
     avg_ms = sum(kern_ms) / len(kern_ms)
     avg_bytes = sum(bytes_per) / len(bytes_per)
     peak, peak_src = measured_peak_hbm()
-    achieved = sum(bytes_per) / (elapsed_ms / 1e3) / 1e9
+    achieved = avg_bytes / (avg_ms / 1e3) / 1e9
+    device_gbs = sum(bytes_per) / (elapsed_ms / 1e3) / 1e9
+    per_lambda = {}
+    for lam in lams:
+        sel = [(f, b) for f, b in zip(fits, bytes_per) if f[0] == lam]
+        ms = sum(f[2] for f, _ in sel) / len(sel)
+        gbs = sel[0][1] / (ms / 1e3) / 1e9
+        per_lambda[f"{lam:.2f}"] = {"ctas": sel[0][0][6], "ms": round(ms, 3), "algorithmic_gb": round(sel[0][1] / 1e9, 2),
+                                    "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    full = {}
+    sf = sched.full
+    sf.set_stream(streams[0].cuda_stream)
+    for lam in (0.30, 0.10):
+        f = one_fit(sf, lam)
+        b = algorithmic_bytes(p, f[3])
+        full[f"{lam:.2f}"] = {"ctas": f[6], "iterations": f[1], "seconds_to_converge": round(f[2] / 1e3, 6),
+                              "gbs": round(b / (f[2] / 1e3) / 1e9, 1), "frac": round(b / (f[2] / 1e3) / 1e9 / peak, 4)}
     workload = f"ar2 p={p} n={n} lambda-path cold"
     traffic = ncu_traffic(workload)
     nnz_frac = [frac(None, f) for f in fits]
@@ -351,9 +408,13 @@ def run_ours(args, d):
         "roofline": {"kernel": kernel, "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
+                     "device_aggregate": {"achieved": device_gbs, "frac": device_gbs / peak,
+                                          "note": "all fits' bytes / the steps' device time (k concurrent launches "
+                                                  "on disjoint SMs): HBM utilisation of the device"},
+                     "per_lambda": per_lambda, "full_device_fits": full,
                      "note": "bytes = sum over sweeps of 48p*nnz_k per colour + 24p per colour + 32p^2 diag/objective"
-                             + "; achieved = all fits' bytes / the device time of the steps (aggregate over "
-                             "concurrent fits)"},
+                             "; achieved = bytes per launch / average launch duration (each launch on its lane's "
+                             "SMs only)"},
         "gpu_launches": 3 * len(fits),
         "clocks": clk,
     }
@@ -362,12 +423,26 @@ def run_ours(args, d):
         out["e2e"] = run_e2e(args, d, s, stream, lams, k)
     if not args.no_cpu and d.world == 1 and d.rank == 0:
         t_host = s.gram().t
-        rate, kind, rounds, el = cpu_reference_rate(t_host, n, 0.3, args.cpu_seconds, os.cpu_count())
-        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
-                               "sample": f"{rounds} of {p + (p % 2) - 1} colour rounds of one pcd_sweep at p={p} "
-                                         f"(workers={os.cpu_count()}), {el:.1f} s; sweep cost is data-independent"}
-        iters_total = sum(f[1] for f in fits)
-        out["cpu_baseline"]["seconds_to_converge_extrapolated"] = iters_total / rate
+        rate, kind, rounds, el, ovh = cpu_reference_rate(t_host, n, 0.3, args.cpu_seconds, os.cpu_count())
+        path_iters = sum(f[1] for f in fits[:len(lams)])  # one step = one path
+        cb_out = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                  "sample": f"{rounds} of {p + (p % 2) - 1} colour rounds of one pcd_sweep at p={p} "
+                            f"(workers={os.cpu_count()}), {el:.1f} s, plus the driver's per-iteration snapshot + "
+                            f"cyclic_max_reduce(_vech) ({ovh:.2f} s, solver.py:283-288); sweep cost is "
+                            f"data-independent",
+                  "path_iterations": path_iters,
+                  "seconds_per_path_extrapolated": path_iters / rate}
+        if args.cpu_validate:
+            v = cpu_full_fit(t_host, n, 0.3, os.cpu_count())
+            v["sampled_per_sweep_s"] = 1.0 / rate
+            v["gpu_iterations"] = dict((f"{f[0]:.2f}", f[1]) for f in fits)["0.30"]
+            cb_out["validation"] = v
+        else:
+            rec = os.path.join(REPO, "profiles", "r02", "cpu_full_fit.json")
+            if os.path.exists(rec):
+                with open(rec) as fh:
+                    cb_out["validation"] = dict(json.load(fh), recorded_in="profiles/r02/cpu_full_fit.json")
+        out["cpu_baseline"] = cb_out
     s.close()
     return out
 
@@ -493,16 +568,17 @@ def run_reference(args, d):
     kind = None
     info = None
     for i in range(W + K):
-        rate, kind, rounds, el = cpu_reference_rate(t, n, LAMS[i % len(LAMS)], per_step, os.cpu_count())
+        rate, kind, rounds, el, ovh = cpu_reference_rate(t, n, LAMS[i % len(LAMS)], per_step, os.cpu_count())
         if i >= W:
-            rates.append((rate, rounds, el))
+            rates.append((rate, rounds, el, ovh))
         info = (rounds, el)
     m_run = p_run + (p_run % 2) - 1
     total_sweeps = sum(r[1] / m_run for r in rates)
-    total_s = sum(r[2] for r in rates)
+    total_s = sum(r[2] + r[3] * r[1] / m_run for r in rates)
     value = total_sweeps / total_s
     sample = (f"each step = {info[0]} colour rounds of the reference pcd_sweep at p={p_run} "
-              f"(compiled _ckernels, workers={os.cpu_count()}); sweeps = rounds/{m_run}")
+              f"(compiled _ckernels, workers={os.cpu_count()}) plus the driver's snapshot + "
+              f"cyclic_max_reduce(_vech) per sweep (solver.py:283-288); sweeps = rounds/{m_run}")
     if p_run != p:
         value *= (p_run / p) ** 3  # the sweep is 16 p^3 bytes of dense dots (_ckernels.pyx:33-36)
         sample += f"; extrapolated to p={p} by (p/{p_run})^3"

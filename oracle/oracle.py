@@ -135,6 +135,35 @@ def vech_max_abs_diff(a, b):
     return lib().oracle_vech_max_abs_diff(_dp(a), _dp(b), a.shape[0])
 
 
+_TRIU = {}
+
+
+def vech(a):
+    """solver.py:181-189 (`_vech`): the stacked upper triangle, by fancy indexing."""
+    p = a.shape[0]
+    if p not in _TRIU:
+        _TRIU.clear()
+        _TRIU[p] = np.triu_indices(p)
+    rows, cols = _TRIU[p]
+    return a[rows, cols]
+
+
+def cyclic_max_reduce(d):
+    """solver.py:141-163: max |d_j| by halving folds (numpy, as the reference runs it)."""
+    work = np.array(d, dtype=np.float64, copy=True).ravel()
+    m = work.shape[0]
+    if m == 1:
+        return float(abs(work[0]))
+    z = (m - 1).bit_length()
+    width = 1 << (z - 1)
+    count = min(width, m - width)
+    work[:count] = np.maximum(np.abs(work[:count]), np.abs(work[width:width + count]))
+    for q in range(z - 2, -1, -1):
+        width = 1 << q
+        work[:width] = np.maximum(np.abs(work[:width]), np.abs(work[width:2 * width]))
+    return float(work[0])
+
+
 def objective(om, t, n, lam):
     """model.py:210-217, verbatim arithmetic."""
     diag = np.diag(om)
@@ -150,11 +179,14 @@ def edge_count(om):
 
 
 def pcd_fit(t, n, lam, delta_tol=1e-5, max_iter=200, workers=1, init=None,
-            trace=True, sweeps=None, use_ref=False):
+            trace=True, sweeps=None, use_ref=False, numpy_delta=False):
     """solver.py:254-294 driver loop over the oracle (or oracle/_ref) sweep.
 
     Returns a dict mirroring FitReport.  ``sweeps`` (a list) receives a copy
-    of the iterate after every sweep when given.
+    of the iterate after every sweep when given.  ``numpy_delta`` computes the
+    convergence metric as the reference does, cyclic_max_reduce(_vech(om -
+    snapshot)) in numpy (solver.py:287), instead of the C scan: the same value,
+    and the reference's own cost inside wall_time_per_iteration.
     """
     t = np.ascontiguousarray(t, np.float64)
     p = t.shape[0]
@@ -175,7 +207,7 @@ def pcd_fit(t, n, lam, delta_tol=1e-5, max_iter=200, workers=1, init=None,
                           ss.astype(np.intp), offsets.astype(np.intp), int(workers))
         else:
             pcd_sweep(om, t, n, float(n) * lam, rs, ss, offsets, workers)
-        delta = vech_max_abs_diff(om, snap)
+        delta = cyclic_max_reduce(vech(om - snap)) if numpy_delta else vech_max_abs_diff(om, snap)
         times.append(time.perf_counter() - tic)
         if trace:
             objs.append(objective(om, t, n, lam))

@@ -130,6 +130,41 @@ def host_gram(x):
     return 0.5 * (raw + raw.T)
 
 
+def quantize_exact_gram(x):
+    """Round X to a 2^-s grid on which X^T X is EXACT in FP64, whatever the summation order.
+
+    With |X| 2^s < 2^a and n < 2^b every product is an integer times 2^-2s below
+    2^2a and every partial sum of n of them stays below 2^(2a+b) <= 2^53, so
+    BLAS (any kernel, any thread count), the GPU's DMMA Gram and a scalar loop
+    all produce the same bits -- T, and every result derived from it, is then
+    portable between this container and the GPU box.  s is the largest such
+    grid for the data (s = 18 for the p=5000, n=2000 AR(2) workload: a step of
+    4e-6 on unit-scale data).
+    """
+    x = np.asarray(x, dtype=np.float64)
+    b = int(np.ceil(np.log2(max(x.shape[0], 2))))
+    a_data = int(np.floor(np.log2(max(float(np.max(np.abs(x))), 1e-300)))) + 1
+    s = (53 - b) // 2 - a_data
+    scale = float(2.0 ** s)
+    return np.ascontiguousarray(np.round(x * scale) / scale), s
+
+
+def portable_problem(kind, p, n, seed=0):
+    """(X, T) with T = X^T X exact in FP64 on every machine (fixtures at configs[1]/[2]).
+
+    X = the reference pipeline center(sample_mvn(truth, n, seed)) rounded onto
+    the exact-Gram grid of `quantize_exact_gram`.  The draws run with one BLAS
+    thread (OpenBLAS's triangular solve splits work by thread count).
+    """
+    from threadpoolctl import threadpool_limits
+
+    truth = ar2_precision(p) if kind == "ar2" else scale_free_precision(p, seed=seed)
+    with threadpool_limits(1):
+        x = center(sample_mvn(truth, n, seed=seed))
+    xq, _ = quantize_exact_gram(x)
+    return xq, host_gram(xq)
+
+
 def problem(kind, p, n, seed=0):
     """(centered X, T) for a truth kind in {"ar2", "scale_free"}."""
     truth = ar2_precision(p) if kind == "ar2" else scale_free_precision(p, seed=seed)

@@ -1,6 +1,8 @@
 """Reference fixtures for the headline workload (BASELINE configs[2]): AR(2), p=5000, n=2000, seed 0.
 
-Run in the build container only (needs /root/reference; about 1 min per sweep on 8 cores):
+Run in the build container (needs /root/reference; about 1 min per sweep on 8 cores) or on
+the GPU box's 16 host cores with the reference staged under baseline/_ref/pkg by
+tools/stage_reference_suite.py (about 12 s per sweep):
 
     python tests/golden/make_golden_p5000.py [lam ...]
 
@@ -8,7 +10,11 @@ For every lambda of the bench path it runs the REAL reference package's stock
 `pcd_fit` loop (`/root/reference/pkg/src/parconcord/solver.py:254-294`) with the
 compiled `_ckernels.pcd_sweep` (`_ckernels.pyx:68-102`), cold from the identity,
 delta_tol 1e-5, on the reference's own generators
-(`datagen.ar2_precision` -> `sample_mvn` -> `center_columns` -> `compute_gram`).
+(`datagen.ar2_precision` -> `sample_mvn` -> `center_columns`), with X rounded
+onto the exact-Gram grid of `synth.quantize_exact_gram` so that T = X^T X is
+the same bits on every machine (BLAS kernel and thread count change the last
+bits of an unrounded Gram); the reference's own `compute_gram` is asserted to
+give exactly that T.
 It writes one compact fixture per lambda to tests/golden/p5000/:
 
 * meta (p, n, lam, delta_tol), sha256 of T (the GPU test regenerates T from the
@@ -34,7 +40,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
-OUT = os.path.join(HERE, "p5000")
+OUT = os.environ.get("P5K_OUT", os.path.join(HERE, "p5000"))
 P, N, TOL = 5000, 2000, 1e-5
 LAMS = [0.30, 0.10, 0.20, 0.15, 0.55, 0.50, 0.45, 0.40, 0.35, 0.25]
 
@@ -62,12 +68,11 @@ def main():
 
     os.makedirs(OUT, exist_ok=True)
     lams = [float(a) for a in sys.argv[1:]] or LAMS
-    truth = pc.ar2_precision(P)
-    gram = pc.compute_gram(pc.center_columns(pc.sample_mvn(truth, N, seed=0)))
-    assert np.array_equal(synth.host_gram(synth.center(synth.sample_mvn(synth.ar2_precision(P), N, seed=0))),
-                          gram.t)
+    x, t = synth.portable_problem("ar2", P, N, seed=0)
+    assert np.array_equal(pc.compute_gram(pc.DataMatrix(x)).t, t)  # the reference's own Gram, bitwise
+    gram = pc.GramMatrix(t, N)
     tsha = sha(gram.t)
-    workers = os.cpu_count()
+    workers = int(os.environ.get("P5K_WORKERS", os.cpu_count()))
     iu = np.triu_indices(P, 1)
     for lam in lams:
         path = fixture_name(lam)

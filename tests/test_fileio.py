@@ -49,6 +49,7 @@ def test_problem_round_trip_is_byte_identical(golden, io_golden, tmp_path):
 @pytest.mark.parametrize("text,msg", [
     ("", "empty"), ("3,1\n", "header"), ("2,2,5\n1,2\n3,4\n", "centered flag"), ("3,2,0\n1,2\n", "promises"),
     ("1,2,0\n1,x\n", "cannot parse"), ("1,3,0\n1,2\n", "expected 3"),
+    ("2,2,0\n1,2\n3,oops\n", ":3: cannot parse value 2"),
 ])
 def test_read_problem_rejects_malformed(tmp_path, text, msg):
     path = tmp_path / "bad.txt"
@@ -61,6 +62,9 @@ def test_read_problem_rejects_malformed(tmp_path, text, msg):
     ("2,0.1,3\n", "header"), ("2,0.1,3,0\n1,1,1\n1,3,0.5\n2,2,1\n", "out of range"),
     ("2,0.1,3,0\n1,1,1\n1,1,1\n2,2,1\n", "duplicate"), ("2,0.1,3,0\n1,1,1\n", "diagonal entry 2"),
     ("2,0.1,3,0\n1,1\n", "expected 'i,j,value'"),
+    ("2,0.1,3,0\n1,1,1\n1,2,x\n2,2,1\n", ":3: cannot parse value"),
+    ("2,0.1,3,0\n1,1,1\n\n1,q,1\n2,2,1\n", ":4: cannot parse j"),
+    ("2,0.1,3,0\n1,1,1\n2,2,1\n1,1,2\n", ":4: duplicate entry \\(1, 1\\)"),
 ])
 def test_read_estimate_rejects_malformed(tmp_path, text, msg):
     path = tmp_path / "bad.txt"

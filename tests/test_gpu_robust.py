@@ -83,3 +83,30 @@ def test_concurrent_pcd_fit_same_p_is_reentrant():
     for i, lam in enumerate(lams):
         assert np.array_equal(got[i], want[lam]), lam
     cb.release_device_memory()
+
+
+def test_path_lanes_with_competing_kernels_on_the_device():
+    """PathScheduler's lanes are cooperative launches sized to fill the device (66/41/41 of 148
+    SMs).  Other work on the GPU -- here 24 single-CTA spin kernels from torch on their own
+    streams, holding 24 SMs for ~1 s, plus a stream of matmuls -- must delay the lanes, never
+    hang them (a partially resident grid would spin at its barrier until the 20 s watchdog
+    traps): every fit still completes with the bits of sequential fits."""
+    import torch
+
+    _, t = synth.problem("ar2", 1000, 500, seed=3)
+    g = cb.GramMatrix(t, 500)
+    lams = [0.3, 0.2, 0.15, 0.1]
+    want = [cb.pcd_fit(g, cb.SolverConfig(lam=lam, max_outer_iterations=5000)) for lam in lams]
+    streams = [torch.cuda.Stream() for _ in range(25)]
+    for s in streams[:24]:
+        with torch.cuda.stream(s):
+            torch.cuda._sleep(int(1.0 * 1.9e9))
+    with torch.cuda.stream(streams[24]):
+        a = torch.randn(4096, 4096, device="cuda")
+        for _ in range(50):
+            a = torch.tanh(a @ a * 1e-3)
+    reps = cb.pcd_path(g, lams, max_outer_iterations=5000, concurrency=3)
+    torch.cuda.synchronize()
+    for r, w in zip(reps, want):
+        assert r.iterations == w.iterations
+        assert np.array_equal(r.estimate.omega, w.estimate.omega)
