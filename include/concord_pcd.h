@@ -118,6 +118,9 @@ void* concord_solver_stream(concord_solver* s);
 int concord_solver_set_gram(concord_solver* s, const double* T, double n, int32_t where);
 /* compute_gram (model.py:190-197) on the device from centred data X (n x p). */
 int concord_solver_gram_from_data(concord_solver* s, const double* X, int64_t n, int32_t where);
+/* center_columns + compute_gram (model.py:182-197; the CLI's load path, cli.py:101-102) on the
+ * device from RAW data X (n x p): the column means are bitwise numpy's x.mean(axis=0). */
+int concord_solver_gram_from_raw_data(concord_solver* s, const double* X, int64_t n, int32_t where);
 int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where);
 /* pcd_fit (solver.py:254-294).  delta_trace / objective_trace / sweep_seconds
  * may be NULL, else hold max_iter doubles.  Returns CONCORD_NOT_CONVERGED when
@@ -179,6 +182,9 @@ int concord_host_free(void* ptr);
 
 /* ---- one-shot conveniences ---------------------------------------------- */
 int concord_gram_f64(const double* X, int64_t n, int64_t p, double* T_out, int32_t device);
+/* center_columns (model.py:182-187) in place on X (n x p row-major, host or device memory per
+ * `where`), bitwise numpy's x - x.mean(axis=0). */
+int concord_center_columns_f64(double* X, int64_t n, int64_t p, int32_t where, int32_t device);
 int concord_pcd_fit(const double* T, int64_t p, double n, const concord_fit_params* prm, double* omega_out,
                     concord_fit_result* res, double* delta_trace, double* objective_trace,
                     double* sweep_seconds, int32_t device);

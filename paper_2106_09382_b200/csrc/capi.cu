@@ -615,6 +615,23 @@ int concord_solver_gram_from_data(concord_solver* s, const double* X, int64_t n,
     return set_gram_rowmajor(s, s->stage, CONCORD_DEVICE);
 }
 
+int concord_solver_gram_from_raw_data(concord_solver* s, const double* X, int64_t n, int32_t where) {
+    if (!s || !X) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (n < 1) return fail(CONCORD_ERR_ARG, "need at least one observation");
+    DeviceGuard g(s->dev);
+    double* tmp = nullptr;
+    CK(dalloc(&tmp, (size_t)n * s->p));
+    cudaError_t e = cudaMemcpyAsync(tmp, X, sizeof(double) * (size_t)n * s->p,
+                                    where == CONCORD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                    s->stream);
+    if (e == cudaSuccess) e = launch_center_columns(tmp, n, s->p, s->p, s->stream);
+    int rc = (e == cudaSuccess) ? concord_solver_gram_from_data(s, tmp, n, CONCORD_DEVICE) : CONCORD_OK;
+    cudaStreamSynchronize(s->stream);
+    cudaFree(tmp);
+    CK(e);
+    return rc;
+}
+
 int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where) {
     if (!s || !T_out) return fail(CONCORD_ERR_ARG, "NULL argument");
     DeviceGuard g(s->dev);
@@ -1126,6 +1143,32 @@ int concord_gram_f64(const double* X, int64_t n, int64_t p, double* T_out, int32
     if (e == cudaSuccess) e = cudaMemcpy(T_out, Td, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost);
     cudaFree(Xd);
     cudaFree(Td);
+    CK(e);
+    return CONCORD_OK;
+}
+
+int concord_center_columns_f64(double* X, int64_t n, int64_t p, int32_t where, int32_t device) {
+    if (!X) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (n < 1) return fail(CONCORD_ERR_ARG, "need at least one observation");
+    if (p < 1 || p > (1LL << 30)) return fail(CONCORD_ERR_ARG, "bad p");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    double* Xd = X;
+    if (where == CONCORD_HOST) {
+        CK(dalloc(&Xd, (size_t)n * p));
+        cudaError_t e = cudaMemcpy(Xd, X, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(Xd);
+            CK(e);
+        }
+    }
+    cudaError_t e = launch_center_columns(Xd, n, (int)p, p, nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (where == CONCORD_HOST) {
+        if (e == cudaSuccess) e = cudaMemcpy(X, Xd, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost);
+        cudaFree(Xd);
+    }
     CK(e);
     return CONCORD_OK;
 }

@@ -119,6 +119,33 @@ __global__ void __launch_bounds__(GTHREADS) gram_f64_kernel(const double* __rest
             }
 }
 
+// center_columns (model.py:182-187: x - x.mean(axis=0)) in place, one thread per column.
+// numpy reduces axis 0 of a C-ordered array row by row (sequential adds into the
+// accumulator row), then divides by n; the same sequential __dadd_rn chain and
+// __ddiv_rn give its bits exactly.  The row loads of a warp are coalesced across
+// columns; eight rows are loaded ahead of the add chain.
+__global__ void center_columns_kernel(double* __restrict__ X, long long n, int p, long long ldx) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p) return;
+    double s = 0.0;
+    long long k = 0;
+    for (; k + 8 <= n; k += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(X + (k + u) * ldx + j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+    }
+    for (; k < n; ++k) s = __dadd_rn(s, __ldcg(X + k * ldx + j));
+    const double mu = __ddiv_rn(s, (double)n);
+    for (k = 0; k < n; ++k) X[k * ldx + j] = __dsub_rn(X[k * ldx + j], mu);
+}
+
+cudaError_t launch_center_columns(double* X, long long n, int p, long long ldx, cudaStream_t st) {
+    center_columns_kernel<<<(p + 127) / 128, 128, 0, st>>>(X, n, p, ldx);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gram_f64(const double* X, long long n, int p, long long ldx, double* out, int out_mode, int w,
                             cudaStream_t st) {
     const int nt = (p + GB - 1) / GB;

@@ -184,6 +184,7 @@ cudaError_t launch_ar2_sample(const double* lb, int p, long long n, unsigned lon
 
 // FP64 DMMA Gram / GEMM, gram.cu.  T = X^T X (X: n x p row-major, leading dim ldx).
 // out_mode 0: row-major p x p (ld = p); 1: slab-major with width w.
+cudaError_t launch_center_columns(double* X, long long n, int p, long long ldx, cudaStream_t st);
 cudaError_t launch_gram_f64(const double* X, long long n, int p, long long ldx, double* out, int out_mode, int w,
                             cudaStream_t st);
 

@@ -216,10 +216,15 @@ class Solver:
                                                       _lib.DEVICE))
         self.n = n
 
-    def gram_from_data(self, x: DataMatrix):
+    def gram_from_data(self, x: DataMatrix, center=False):
+        """compute_gram (model.py:190-197) of X as given, like the reference (callers own centering);
+        center=True first runs center_columns on the device (bitwise numpy's, model.py:182-187) unless
+        the DataMatrix is marked centred -- the CLI's load path (cli.py:101-102) without a host pass."""
         if x.p != self.p:
             raise DimensionError(f"solver has p={self.p} but data has p={x.p}")
-        _lib.check(_lib.load().concord_solver_gram_from_data(self._h, _lib.ptr(x.values), x.n, _lib.HOST))
+        center = bool(center) and not x.centered
+        fn = _lib.load().concord_solver_gram_from_raw_data if center else _lib.load().concord_solver_gram_from_data
+        _lib.check(fn(self._h, _lib.ptr(x.values), x.n, _lib.HOST))
         self.n = x.n
 
     def gram_from_ar2(self, n, seed=0):

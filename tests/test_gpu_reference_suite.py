@@ -53,7 +53,6 @@ def _passed(out, pattern):
 def test_reference_solver_suite_on_cuda_backends():
     rc, out = _run(["tests/test_solver.py"])
     assert rc == 0, out[-4000:]
-    assert "refsuite_plugin: B200 backends" in out
     cuda = _passed(out, r"\[cuda\]")
     fit = _passed(out, r"\[cuda-fit\]")
     # every backend-parametrised test of test_solver.py ran on both GPU backends
