@@ -153,6 +153,14 @@ int concord_solver_sweep_stats(concord_solver* s, int64_t* nnz_pairs, int32_t ca
  * stream, O(p n) work, no host copy of X when the Gram is built in place. */
 int concord_ar2_data_f64(int64_t p, int64_t n, uint64_t seed, double* X_out, int32_t where, int32_t device);
 int concord_solver_gram_from_ar2(concord_solver* s, int64_t n, uint64_t seed);
+/* Scale-free truth (datagen.py:99-132): centred N(0, inv(truth)) samples for a tree-structured
+ * truth given by its fill-free Cholesky factor in leaves-first order -- parent[v] < v
+ * (parent[0] = -1), L[v,v] = ldiag[v], L[parent[v], v] = lpar[v] (synth.tree_cholesky) --
+ * drawn on the device (Philox) in O(p n); the solver variant builds T in place. */
+int concord_tree_data_f64(int64_t p, int64_t n, uint64_t seed, const int32_t* parent, const double* lpar,
+                          const double* ldiag, double* X_out, int32_t where, int32_t device);
+int concord_solver_gram_from_tree(concord_solver* s, int64_t n, uint64_t seed, const int32_t* parent,
+                                  const double* lpar, const double* ldiag);
 
 /* ---- pinned host buffers for fast H2D/D2H of T and Omega ---------------- */
 /* Kernel plan the library chooses for a p x p problem on one device with n_sms SMs (one CTA per

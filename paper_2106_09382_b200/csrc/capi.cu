@@ -1050,9 +1050,66 @@ int ar2_sample_device(int p, long long n, unsigned long long seed, double* X_dev
     return CONCORD_OK;
 }
 
+// Tree-structured truth (scale-free): parent/lpar/ldiag host arrays of p entries (synth.tree_cholesky).
+int tree_sample_device(int p, long long n, unsigned long long seed, const int32_t* parent, const double* lpar,
+                       const double* ldiag, double* X_dev, cudaStream_t st) {
+    for (int v = 0; v < p; ++v) {
+        if (parent[v] >= v || (v > 0 && parent[v] < 0) || (v == 0 && parent[v] != -1))
+            return fail(CONCORD_ERR_ARG, "parent[%d] = %d: need parent[0] = -1 and 0 <= parent[v] < v", v, parent[v]);
+        if (!(ldiag[v] > 0.0)) return fail(CONCORD_ERR_ARG, "ldiag[%d] must be positive", v);
+    }
+    int* dpar = nullptr;
+    double *dl = nullptr, *XT = nullptr, *mean = nullptr;
+    cudaError_t e = cudaMalloc(&dpar, sizeof(int) * (size_t)p);
+    if (e == cudaSuccess) e = dalloc(&dl, 2 * (size_t)p);
+    if (e == cudaSuccess) e = dalloc(&XT, (size_t)n * p);
+    if (e == cudaSuccess) e = dalloc(&mean, p);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dpar, parent, sizeof(int) * (size_t)p, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dl, lpar, sizeof(double) * (size_t)p, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dl + p, ldiag, sizeof(double) * (size_t)p, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch_tree_sample(dpar, dl, dl + p, p, n, seed, XT, mean, X_dev, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dpar);
+    cudaFree(dl);
+    cudaFree(XT);
+    cudaFree(mean);
+    CK(e);
+    return CONCORD_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int concord_tree_data_f64(int64_t p, int64_t n, uint64_t seed, const int32_t* parent, const double* lpar,
+                          const double* ldiag, double* X_out, int32_t where, int32_t device) {
+    if (!X_out || !parent || !lpar || !ldiag || p < 2 || p > (1LL << 30) || n < 1)
+        return fail(CONCORD_ERR_ARG, "need p >= 2, n >= 1 and non-NULL buffers");
+    int rc = check_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    double* Xd = X_out;
+    if (where == CONCORD_HOST) CK(dalloc(&Xd, (size_t)n * p));
+    rc = tree_sample_device((int)p, n, seed, parent, lpar, ldiag, Xd, nullptr);
+    if (!rc && where == CONCORD_HOST) {
+        cudaError_t e = cudaMemcpy(X_out, Xd, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = fail(CONCORD_ERR_CUDA, "copy: %s", cudaGetErrorString(e));
+    }
+    if (where == CONCORD_HOST) cudaFree(Xd);
+    return rc;
+}
+
+int concord_solver_gram_from_tree(concord_solver* s, int64_t n, uint64_t seed, const int32_t* parent,
+                                  const double* lpar, const double* ldiag) {
+    if (!s || n < 1 || !parent || !lpar || !ldiag) return fail(CONCORD_ERR_ARG, "bad arguments");
+    DeviceGuard g(s->dev);
+    double* X = nullptr;
+    CK(dalloc(&X, (size_t)n * s->p));
+    int rc = tree_sample_device(s->p, n, seed, parent, lpar, ldiag, X, s->stream);
+    if (!rc) rc = concord_solver_gram_from_data(s, X, n, CONCORD_DEVICE);
+    cudaFree(X);
+    return rc;
+}
 
 int concord_ar2_data_f64(int64_t p, int64_t n, uint64_t seed, double* X_out, int32_t where, int32_t device) {
     if (!X_out || p < 3 || n < 1) return fail(CONCORD_ERR_ARG, "need p >= 3, n >= 1 and an output buffer");

@@ -36,6 +36,28 @@ __global__ void ar2_sample_kernel(const double* __restrict__ lb, int p, long lon
     }
 }
 
+// Scale-free truth (datagen.py:99-132): a preferential-attachment TREE plus the unit diagonal,
+// where every vertex v >= 1 attaches to an earlier vertex parent[v] < v.  Eliminating leaves
+// first (decreasing index) factors the truth with no fill: L[v,v] = ldiag[v] and the only
+// sub-diagonal entry of column v is L[parent[v], v] = lpar[v] (host: synth.tree_cholesky).
+// L^T x = z is then one recurrence per sample from the root down:
+//     x_v = (z_v - lpar[v] * x_parent[v]) / ldiag[v],  v = 0 .. p-1   (parent[0] = -1)
+// The parent's value of the same sample is read back from XT (sample-minor, coalesced).
+__global__ void tree_sample_kernel(const int* __restrict__ parent, const double* __restrict__ lpar,
+                                   const double* __restrict__ ldiag, int p, long long n, unsigned long long seed,
+                                   double* __restrict__ XT) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    curandStatePhilox4_32_10_t rng;
+    curand_init(seed, (unsigned long long)t, 0ull, &rng);
+    for (int v = 0; v < p; ++v) {
+        const double z = curand_normal_double(&rng);
+        const int u = __ldg(parent + v);
+        const double xp = (u >= 0) ? XT[(long long)u * n + t] : 0.0;
+        XT[(long long)v * n + t] = (z - __ldg(lpar + v) * xp) / __ldg(ldiag + v);
+    }
+}
+
 // Mean over the n samples of every variable (row i of XT), two-level sum in double.
 __global__ void row_mean_kernel(const double* __restrict__ XT, int p, long long n, double* __restrict__ mean) {
     __shared__ double sred[32];
@@ -76,6 +98,19 @@ __global__ void transpose_center_kernel(const double* __restrict__ XT, const dou
 cudaError_t launch_ar2_sample(const double* lb, int p, long long n, unsigned long long seed, double* XT, double* mean,
                               double* X, cudaStream_t st) {
     ar2_sample_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(lb, p, n, seed, XT);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    row_mean_kernel<<<p < 148 * 8 ? p : 148 * 8, 256, 0, st>>>(XT, p, n, mean);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    transpose_center_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((p + 31) / 32)), dim3(32, 8), 0, st>>>(
+        XT, mean, p, n, X);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tree_sample(const int* parent, const double* lpar, const double* ldiag, int p, long long n,
+                               unsigned long long seed, double* XT, double* mean, double* X, cudaStream_t st) {
+    tree_sample_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(parent, lpar, ldiag, p, n, seed, XT);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     row_mean_kernel<<<p < 148 * 8 ? p : 148 * 8, 256, 0, st>>>(XT, p, n, mean);

@@ -179,6 +179,8 @@ cudaError_t launch_triplet_write(const double* Om, int p, int w, const long long
                                  double* tv, cudaStream_t st);
 
 // On-device AR(2) samples (datagen.cu): centred X (n x p row-major); XT (p x n) and mean (p) are scratch.
+cudaError_t launch_tree_sample(const int* parent, const double* lpar, const double* ldiag, int p, long long n,
+                               unsigned long long seed, double* XT, double* mean, double* X, cudaStream_t st);
 cudaError_t launch_ar2_sample(const double* lb, int p, long long n, unsigned long long seed, double* XT, double* mean,
                               double* X, cudaStream_t st);
 

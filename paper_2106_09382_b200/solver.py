@@ -232,6 +232,17 @@ class Solver:
         _lib.check(_lib.load().concord_solver_gram_from_ar2(self._h, int(n), int(seed)))
         self.n = int(n)
 
+    def gram_from_scale_free(self, n, seed=0, alpha=2.3, truth_seed=None):
+        """T of n centred samples of the scale-free truth (datagen.py:99-132), drawn on the device
+        through the truth's fill-free tree Cholesky factor (no dense p x p truth, no host copy of X)."""
+        from .synth import scale_free_tree, tree_cholesky
+
+        parent, weight = scale_free_tree(self.p, alpha, seed if truth_seed is None else truth_seed)
+        lpar, ldiag = tree_cholesky(parent, weight)
+        _lib.check(_lib.load().concord_solver_gram_from_tree(self._h, int(n), int(seed), _lib.ptr(parent),
+                                                             _lib.ptr(lpar), _lib.ptr(ldiag)))
+        self.n = int(n)
+
     def gram(self) -> GramMatrix:
         t = np.empty((self.p, self.p))
         _lib.check(_lib.load().concord_solver_get_gram(self._h, _lib.ptr(t), _lib.HOST))

@@ -67,6 +67,87 @@ def scale_free_precision(p, alpha=2.3, seed=0):
     return b
 
 
+def scale_free_tree(p, alpha=2.3, seed=0):
+    """The scale-free truth of datagen.py:99-132 in O(p) memory: (parent, weight).
+
+    The same attachment tree (datagen.py:81-96, the reference's RNG streams, so the
+    same edges, magnitudes and signs bit for bit) and the same scaling
+    u / (1.25 sqrt(r_i r_j)) with the 0.1 magnitude floor; vertex v >= 1 hangs
+    off parent[v] < v with truth[v, parent[v]] = weight[v] (parent[0] = -1,
+    unit diagonal).  The row sums r are accumulated edge by edge instead of as
+    numpy's dense row sums, so a value may differ from scale_free_precision's
+    in the last bit; the support is identical.  For p where the dense p x p
+    truth does not fit (configs[4]).
+    """
+    if p < 3:
+        raise ValueError("scale-free truth needs p >= 3")
+    graph_seed, weight_seed = np.random.SeedSequence(seed).spawn(2)
+    rng_graph = np.random.default_rng(graph_seed)
+    rng_weight = np.random.default_rng(weight_seed)
+    edges = np.asarray(_attachment_edges(p, alpha, rng_graph), dtype=np.int64)  # (u, v), u < v; edge k -> v = k+1
+    mags = rng_weight.uniform(0.5, 1.0, size=len(edges))
+    signs = rng_weight.choice([-1.0, 1.0], size=len(edges))
+    u = mags * signs
+    r = np.zeros(p)
+    np.add.at(r, edges[:, 0], np.abs(u))
+    np.add.at(r, edges[:, 1], np.abs(u))
+    b = u / (1.25 * np.sqrt(r[edges[:, 0]] * r[edges[:, 1]]))
+    small = np.abs(b) < 0.1
+    b[small] = 0.1 * np.sign(b[small])
+    parent = np.full(p, -1, dtype=np.int32)
+    weight = np.zeros(p)
+    parent[edges[:, 1]] = edges[:, 0]
+    weight[edges[:, 1]] = b
+    return parent, weight
+
+
+def tree_cholesky(parent, weight):
+    """Fill-free Cholesky of a tree truth (unit diagonal, truth[v, parent[v]] = weight[v]).
+
+    With parent[v] < v, eliminating leaves first (decreasing v) creates no fill:
+    L[v, v] = ldiag[v] and column v's only sub-diagonal entry is
+    L[parent[v], v] = lpar[v]; truth = L L^T in that order.  Raises
+    NotPositiveDefinite like sample_mvn (datagen.py:146-151).
+    """
+    p = parent.shape[0]
+    d = np.ones(p)
+    ldiag = np.zeros(p)
+    lpar = np.zeros(p)
+    for v in range(p - 1, -1, -1):
+        if not d[v] > 0.0:
+            raise NotPositiveDefinite("truth is not positive definite")
+        ldiag[v] = np.sqrt(d[v])
+        if parent[v] >= 0:
+            lpar[v] = weight[v] / ldiag[v]
+            d[parent[v]] -= lpar[v] * lpar[v]
+    return lpar, ldiag
+
+
+def tree_dense(parent, weight):
+    """The dense p x p truth of a tree (small p, tests)."""
+    p = parent.shape[0]
+    om = np.eye(p)
+    v = np.flatnonzero(parent >= 0)
+    om[v, parent[v]] = om[parent[v], v] = weight[v]
+    return om
+
+
+def sample_scale_free_device(p, n, seed=0, alpha=2.3, truth_seed=None, device=0):
+    """Centred N(0, inv(scale-free truth)) samples drawn on the GPU (csrc/datagen.cu tree sampler).
+
+    Same distribution as center(sample_mvn(scale_free_precision(p, alpha, truth_seed), n, seed));
+    a different (Philox) random stream, O(p n) work, no dense p x p Cholesky.
+    """
+    from . import _lib
+
+    parent, weight = scale_free_tree(p, alpha, seed if truth_seed is None else truth_seed)
+    lpar, ldiag = tree_cholesky(parent, weight)
+    x = np.empty((n, p))
+    _lib.check(_lib.load().concord_tree_data_f64(int(p), int(n), int(seed), _lib.ptr(parent), _lib.ptr(lpar),
+                                                 _lib.ptr(ldiag), _lib.ptr(x), _lib.HOST, int(device)))
+    return x
+
+
 def sample_mvn(omega_true, n, seed=0):
     """datagen.py:135-154: n rows of N(0, inv(omega_true)), raw (uncentered)."""
     try:

@@ -109,3 +109,37 @@ def test_path_scheduler_lanes_fall_back_when_memory_is_short():
         assert len(sched.shares) == (3 if sched.k == 3 else 0)
     finally:
         sched.close()
+
+
+def test_device_scale_free_sampler_moments():
+    """synth.sample_scale_free_device (csrc/datagen.cu tree sampler) draws N(0, inv(truth)) for the
+    scale-free truth of datagen.py:99-132: centred, sample covariance within sampling error of the
+    truth's inverse, reproducible per seed; Solver.gram_from_scale_free builds T of the same draws."""
+    p, n = 60, 200_000
+    x = synth.sample_scale_free_device(p, n, seed=5, truth_seed=0)
+    assert x.shape == (n, p)
+    assert np.max(np.abs(x.mean(axis=0))) < 1e-12
+    parent, weight = synth.scale_free_tree(p, seed=0)
+    sigma = np.linalg.inv(synth.tree_dense(parent, weight))
+    np.testing.assert_allclose(synth.tree_dense(parent, weight), synth.scale_free_precision(p, seed=0), rtol=2e-15)
+    s = x.T @ x / n
+    assert np.max(np.abs(s - sigma)) < 6.0 * np.max(np.abs(sigma)) / np.sqrt(n)
+    assert np.array_equal(x, synth.sample_scale_free_device(p, n, seed=5, truth_seed=0))
+    with cb.Solver(p) as s1:
+        s1.gram_from_scale_free(n, seed=5, truth_seed=0)
+        g = s1.gram()
+    np.testing.assert_allclose(g.t, synth.host_gram(x), rtol=1e-12, atol=1e-9)
+
+
+def test_scale_free_large_p_on_device():
+    """Scale-free data at a size where the dense truth and its Cholesky are the host bottleneck
+    (p=10000, n=5000: drawn and reduced on the device), then a lambda=0.3 fit.  At p=20000 the
+    reference's own truth (seed 0) is not positive definite -- its sample_mvn raises
+    NotPositiveDefinite (datagen.py:146-151) -- and so does the tree factorisation."""
+    with cb.Solver(10000) as s:
+        s.gram_from_scale_free(5000, seed=0)
+        assert np.all(np.diagonal(s.gram().t) > 0)
+        rep = s.fit(0.3, 1e-5, 200)
+        assert rep.converged and np.array_equal(rep.estimate.omega, rep.estimate.omega.T)
+    with pytest.raises(synth.NotPositiveDefinite):
+        synth.tree_cholesky(*synth.scale_free_tree(20000, seed=0))
