@@ -299,8 +299,15 @@ static bool qblock_plan(int p, int nblk, int share, int D, bool allow_overlap, Q
     if (D < 2) D = 2;
     if (D > QB_DMAX) D = QB_DMAX;
     if (2 * D > m + 1) D = (m + 1) / 2;
-    const int pf_threads = 32 * (WFORM_CHAIN_WARPS_QB - qblock_colour_warps(share, D));
-    const bool can_overlap = allow_overlap && pf_threads > 0 && qblock_cellcap(share, D) <= 5 * pf_threads;
+    int cw = qblock_colour_warps(share, D);
+    if (const char* e = getenv("CONCORD_QB_CW")) {  // tuning: a negative value fixes the colour group's warps
+        const int v = atoi(e);
+        cw = v < 0 ? -v : (v > cw ? v : cw);
+    }
+    int pf_cells = 5;  // part A overlaps the colours when the prefetch group has at most this many cells per thread
+    if (const char* e = getenv("CONCORD_QB_PF_CELLS")) pf_cells = atoi(e);
+    const int pf_threads = 32 * (WFORM_CHAIN_WARPS_QB - cw);
+    const bool can_overlap = allow_overlap && pf_threads > 0 && qblock_cellcap(share, D) <= pf_cells * pf_threads;
     static const int plans[][3] = {{2, 1, 6}, {2, 0, 6}, {1, 1, 6}, {1, 0, 6}, {1, 0, 4}, {1, 0, 2}};
     const int td_ok = wform_tdiag_in_smem(p);
     for (const auto& pl : plans) {

@@ -499,7 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         // prefetch group) meanwhile build part A of the next block's cells, so only part B
         // (the previous block's deltas) is left between a barrier and the colours.  When the
         // colours need every chain warp, part A runs after the arrive instead.
-        const int ncw0 = max(colour_warps(a.share, D), min(a.colour_warps_min, kChainWarps));
+        // colour_warps_min < 0: exactly -colour_warps_min warps (tuning; the colours loop over pairs)
+        const int ncw0 = (a.colour_warps_min < 0) ? min(-a.colour_warps_min, kChainWarps)
+                                                  : max(colour_warps(a.share, D), min(a.colour_warps_min, kChainWarps));
         const bool overlap = ncw0 < kChainWarps && a.nbuf == 2;
         const int ncw = overlap ? ncw0 : kChainWarps;
         const int cg0 = kChain - 32 * ncw;  // first thread of the colour group
