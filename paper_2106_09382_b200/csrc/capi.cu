@@ -66,13 +66,17 @@ int check_device(int32_t device) {
 
 // Byte offsets of the exchange buffers inside one arena (identical on every shard).
 struct ArenaLayout {
-    size_t pub, dring, list_rs, list_dn, list_cnt, bar, dmax, bytes;
+    size_t pub, dring, list_rs, list_dn, list_cnt, bar, dmax;
+    // the blocked kernel's exchange buffers (pcd_qblock.cu), present when qb_sr > 0
+    size_t qb_stW, qb_stO, qb_stT, qb_diagv, qb_dring, qb_lrs, qb_ldn, qb_lcnt;
+    size_t bytes;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-ArenaLayout arena_layout(int p, int rd, int rl, int nblk_tot, int share) {
-    ArenaLayout L;
+ArenaLayout arena_layout(int p, int rd, int rl, int nblk_tot, int share, int qb_sr = 0, int qb_rd = 0,
+                         int qb_rl = 0) {
+    ArenaLayout L{};
     size_t o = 0;
     L.pub = o;
     o = align256(o + sizeof(double2) * 3 * (size_t)p);
@@ -88,6 +92,24 @@ ArenaLayout arena_layout(int p, int rd, int rl, int nblk_tot, int share) {
     o = align256(o + sizeof(unsigned long long));
     L.dmax = o;
     o = align256(o + sizeof(unsigned long long) * WFORM_DMAX_RING);
+    if (qb_sr > 0) {
+        L.qb_stW = o;
+        o = align256(o + sizeof(double) * (size_t)qb_sr * p);
+        L.qb_stO = o;
+        o = align256(o + sizeof(double) * (size_t)qb_sr * p);
+        L.qb_stT = o;
+        o = align256(o + sizeof(double) * (size_t)qb_sr * (QB_DMAX - 1) * p);
+        L.qb_diagv = o;
+        o = align256(o + sizeof(double2) * (size_t)p);
+        L.qb_dring = o;
+        o = align256(o + sizeof(double) * (size_t)qb_rd * p);
+        L.qb_lrs = o;
+        o = align256(o + sizeof(int2) * (size_t)qb_rl * nblk_tot * share);
+        L.qb_ldn = o;
+        o = align256(o + sizeof(double2) * (size_t)qb_rl * nblk_tot * share);
+        L.qb_lcnt = o;
+        o = align256(o + sizeof(int) * (size_t)qb_rl * nblk_tot);
+    }
     L.bytes = o;
     return L;
 }
@@ -109,14 +131,7 @@ struct concord_solver {
     bool qb = false;       // temporally blocked chain (pcd_qblock.cu)
     int qb_D = 0, qb_NB = 0, qb_sr = 0, qb_rd = 0, qb_rl = 0;
     int qb_nbuf = 1, qb_td = 0, qb_ring = 6;  // shared-memory plan of the blocked kernel
-    double* qb_stW = nullptr;
-    double* qb_stO = nullptr;
-    double* qb_stT = nullptr;
-    double2* qb_diagv = nullptr;
-    double* qb_dring = nullptr;
-    int2* qb_lrs = nullptr;
-    double2* qb_ldn = nullptr;
-    int* qb_lcnt = nullptr;
+    double* Tfull = nullptr;  // process shard on the blocked kernel: every slab of T (the cells' T entries)
     long long* hang = nullptr;  // mapped host memory: the fit kernels' watchdog report
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -191,6 +206,7 @@ int set_gram_rowmajor(concord_solver* s, const double* src, int32_t where) {
         dsrc = s->stage;
     }
     CK(launch_pack_slabs(dsrc, s->p, s->T, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
+    if (s->Tfull) CK(launch_pack_slabs(dsrc, s->p, s->Tfull, s->p, s->w, s->nblk_tot, 0, s->stream));
     CK(launch_rowmajor_diag(dsrc, s->tdiag, s->p, s->stream));
     std::vector<double> d(s->p);
     CK(cudaMemcpyAsync(d.data(), s->tdiag, sizeof(double) * s->p, cudaMemcpyDeviceToHost, s->stream));
@@ -322,7 +338,8 @@ static bool qblock_plan(int p, int nblk, int share, int D, bool allow_overlap, Q
     return false;
 }
 
-// Buffers of the temporally blocked chain (pcd_qblock.cu); leaves s->qb false when it does not fit.
+// Plan of the temporally blocked chain (pcd_qblock.cu); leaves s->qb false when it does not fit.
+// Its exchange buffers are carved from the shard arenas (arena_layout) by create_common.
 int setup_qblock(concord_solver* s) {
     const int p = s->p;
     const int m = p + (p & 1) - 1;
@@ -347,14 +364,6 @@ int setup_qblock(concord_solver* s) {
     s->qb_sr = 4 * D + 4;
     s->qb_rd = 8 * D + 8;
     s->qb_rl = 10 * D + 8;
-    CK(dalloc(&s->qb_stW, (size_t)s->qb_sr * p));
-    CK(dalloc(&s->qb_stO, (size_t)s->qb_sr * p));
-    CK(dalloc(&s->qb_stT, (size_t)s->qb_sr * (QB_DMAX - 1) * p));
-    CK(dalloc(&s->qb_diagv, p));
-    CK(dalloc(&s->qb_dring, (size_t)s->qb_rd * p));
-    CK(dalloc(&s->qb_lrs, (size_t)s->qb_rl * s->nblk_tot * s->share));
-    CK(dalloc(&s->qb_ldn, (size_t)s->qb_rl * s->nblk_tot * s->share));
-    CK(dalloc(&s->qb_lcnt, (size_t)s->qb_rl * s->nblk_tot));
     s->qb = true;
     return CONCORD_OK;
 }
@@ -442,7 +451,19 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
         s->lmax = wform_lag_cap(w, 2 * half - 1);
         s->rd = s->lmax + 3;
         s->rl = s->lmax + 4;
-        s->L = arena_layout(ip, s->rd, s->rl, s->nblk_tot, s->share);
+    }
+    // the temporally blocked kernel (default for p >= 256, every shard layout); CONCORD_KERNEL=wform
+    // selects the per-phase one
+    {
+        bool use_qb = ip >= 256;
+        if (const char* e = getenv("CONCORD_KERNEL")) use_qb = use_qb && strcmp(e, "qblock") == 0;
+        else use_qb = use_qb && QB_DEFAULT;
+        if (use_qb) {
+            const int rc = setup_qblock(s);
+            if (rc) return cleanup(rc);
+        }
+        s->L = s->qb ? arena_layout(ip, s->rd, s->rl, s->nblk_tot, s->share, s->qb_sr, s->qb_rd, s->qb_rl)
+                     : arena_layout(ip, s->rd, s->rl, s->nblk_tot, s->share);
     }
     for (int r = 0; r < G; ++r) {
         if (rank >= 0 && r != rank) continue;  // peers' arenas are opened by concord_shard_open_peers
@@ -454,18 +475,12 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
     CKC(dalloc(&s->edges, 1));
     CKC(dalloc(&s->status, 2));
     for (auto& e : s->ev) CKC(cudaEventCreate(&e));
+    if (s->qb && rank >= 0 && G > 1) {  // the cells read T entries of every column
+        CKC(dalloc(&s->Tfull, (size_t)s->nblk_tot * s->slab));
+        CKC(cudaMemsetAsync(s->Tfull, 0, sizeof(double) * (size_t)s->nblk_tot * s->slab, s->stream));
+    }
     CKC(cudaStreamSynchronize(s->stream));
 #undef CKC
-    // temporally blocked chain for the single-device unsharded solver
-    // the blocked kernel for single-device solvers (also with an explicit slab count: a fit on a
-    // share of the SMs, e.g. concurrent lambda fits); CONCORD_KERNEL=wform selects the per-phase one
-    bool use_qb = (G == 1 && rank < 0 && ip >= 256);
-    if (const char* e = getenv("CONCORD_KERNEL")) use_qb = use_qb && strcmp(e, "qblock") == 0;
-    else use_qb = use_qb && QB_DEFAULT;
-    if (use_qb) {
-        const int rc = setup_qblock(s);
-        if (rc) return cleanup(rc);
-    }
     *out = s;
     return CONCORD_OK;
 }
@@ -554,14 +569,7 @@ int concord_solver_destroy(concord_solver* s) {
     cudaFree(s->tdiag);
     cudaFree(s->stage);
     cudaFree(s->diagd);
-    cudaFree(s->qb_stW);
-    cudaFree(s->qb_stO);
-    cudaFree(s->qb_stT);
-    cudaFree(s->qb_diagv);
-    cudaFree(s->qb_dring);
-    cudaFree(s->qb_lrs);
-    cudaFree(s->qb_ldn);
-    cudaFree(s->qb_lcnt);
+    cudaFree(s->Tfull);
     for (int r = 0; r < WFORM_MAX_SHARDS; ++r) {
         if (!s->arena[r]) continue;
         if (s->arena_owned[r]) cudaFree(s->arena[r]);
@@ -690,6 +698,8 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     a.nblk_tot = s->nblk_tot;
     a.blk0 = s->blk0;
     a.sys_scope = (s->rank >= 0 && s->G > 1) ? 1 : 0;
+    // testing: the system-scope (NVLink peer) fences and reductions on virtual shards of one device
+    if (const char* e = getenv("CONCORD_FORCE_SYS_SCOPE")) a.sys_scope = atoi(e) ? 1 : a.sys_scope;
     a.bar_base = s->bar_base;
     a.it_base = s->it_base;
     a.n = s->n;
@@ -730,6 +740,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.slab = a.slab;
         q.W = a.W;
         q.T = a.T;
+        q.Tfull = s->Tfull ? s->Tfull : a.T;
         q.Om = a.Om;
         q.tdiag = a.tdiag;
         q.tdiag_smem = s->qb_td;
@@ -737,20 +748,28 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.colour_warps_min = 1;
         if (const char* e = getenv("CONCORD_QB_CW")) q.colour_warps_min = atoi(e);
         q.ring_stages = s->qb_ring;
-        q.diagv = s->qb_diagv;
-        q.stW = s->qb_stW;
-        q.stO = s->qb_stO;
-        q.stT = s->qb_stT;
+        for (int r = 0; r < s->G; ++r) {
+            char* base = static_cast<char*>(s->arena[r]);
+            q.x.diagv[r] = reinterpret_cast<double2*>(base + s->L.qb_diagv);
+            q.x.stW[r] = reinterpret_cast<double*>(base + s->L.qb_stW);
+            q.x.stO[r] = reinterpret_cast<double*>(base + s->L.qb_stO);
+            q.x.stT[r] = reinterpret_cast<double*>(base + s->L.qb_stT);
+            q.x.dring[r] = reinterpret_cast<double*>(base + s->L.qb_dring);
+            q.x.list_rs[r] = reinterpret_cast<int2*>(base + s->L.qb_lrs);
+            q.x.list_dn[r] = reinterpret_cast<double2*>(base + s->L.qb_ldn);
+            q.x.list_cnt[r] = reinterpret_cast<int*>(base + s->L.qb_lcnt);
+            q.x.bar[r] = a.x.bar[r];
+            q.x.dmax[r] = a.x.dmax[r];
+        }
+        q.G = s->G;
+        q.nblk_loc = s->nblk_loc;
+        q.nblk_tot = s->nblk_tot;
+        q.blk0 = s->blk0;
+        q.sys_scope = a.sys_scope;
         q.sr = s->qb_sr;
-        q.dring = s->qb_dring;
         q.rd = s->qb_rd;
-        q.list_rs = s->qb_lrs;
-        q.list_dn = s->qb_ldn;
-        q.list_cnt = s->qb_lcnt;
         q.rl = s->qb_rl;
         q.share = s->share;
-        q.bar = a.x.bar[0];
-        q.dmax = a.x.dmax[0];
         q.bar_base = a.bar_base;
         q.it_base = a.it_base;
         q.n = a.n;

@@ -336,8 +336,26 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
 #define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) \
     apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_, a.ring_stages)
 
+#define QB_COPIES(r) _Pragma("unroll") for (int r = 0; r < WFORM_MAX_SHARDS; ++r) if (r < a.G)
+
+// Arrive on the grid barrier of every shard: this CTA's exchange-buffer stores (its own and, through
+// the CTA barrier before the call, its other threads') become visible at GPU scope -- or system
+// scope when the shards are separate GPUs reached over NVLink -- then every copy of the counter
+// is bumped.  One GPU, one copy: a release reduction (no separate fence).
+__device__ __forceinline__ void qb_arrive(const QbArgs& a) {
+    if (a.sys_scope) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        QB_COPIES(r) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
+    } else if (a.G == 1) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[0]) : "memory");
+    } else {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        QB_COPIES(r) asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
+    }
+}
+
 __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsigned long long target, int blk,
-                                             long long* hang) {
+                                             long long* hang, int sys) {
     unsigned long long v;
     const unsigned long long t0 = globaltimer_ns();
     int spins = 0;
@@ -349,7 +367,8 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsi
             if (globaltimer_ns() - t0 > kHangNs) hang_report(hang, 0, blk, (long long)v, (long long)target, 0, 0);
         }
     } while (v < target);
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 struct Layout {
@@ -415,19 +434,44 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     __shared__ double s_red[4][kApplyWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.x, bl = b, nblk = gridDim.x;
+    const int bl = blockIdx.x;       // slab of this launch
+    const int b = a.blk0 + bl;       // global CTA = global column block (pairs, list segments)
+    const int nblk = a.nblk_tot;     // CTAs over all shards
+    const int shard = b / a.nblk_loc;  // whose copy of the exchange buffers this CTA reads
     const int p = a.p, m = a.m, w = a.w, w2 = a.w >> 1, half = a.half;
     const int D = a.D, NB = a.NB;
     const int dm1 = D - 1;  // stride of the per-cell arrays cT, cQ
     const int c0 = b * w;
     const int wl = max(0, min(w, p - c0));
     const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
-    double* __restrict__ Wb = a.W + (long long)b * a.slab;
-    const double* __restrict__ Tb = a.T + (long long)b * a.slab;
-    double* __restrict__ Ob = a.Om + (long long)b * a.slab;
-    const int* lcntL = a.list_cnt;
-    const int2* lrsL = a.list_rs;
-    const double2* ldnL = a.list_dn;
+    double* __restrict__ Wb = a.W + (long long)bl * a.slab;
+    const double* __restrict__ Tb = a.T + (long long)bl * a.slab;
+    double* __restrict__ Ob = a.Om + (long long)bl * a.slab;
+    // this shard's copies (read side); every write goes to all copies (QB_COPIES)
+    const int* lcntL = a.x.list_cnt[0];
+    const int2* lrsL = a.x.list_rs[0];
+    const double2* ldnL = a.x.list_dn[0];
+    const double* stWL = a.x.stW[0];
+    const double* stOL = a.x.stO[0];
+    const double* stTL = a.x.stT[0];
+    const double* dringL = a.x.dring[0];
+    const double2* diagvL = a.x.diagv[0];
+    const unsigned long long* barL = a.x.bar[0];
+    const unsigned long long* dmaxL = a.x.dmax[0];
+#pragma unroll
+    for (int r = 1; r < WFORM_MAX_SHARDS; ++r)
+        if (r == shard) {
+            lcntL = a.x.list_cnt[r];
+            lrsL = a.x.list_rs[r];
+            ldnL = a.x.list_dn[r];
+            stWL = a.x.stW[r];
+            stOL = a.x.stO[r];
+            stTL = a.x.stT[r];
+            dringL = a.x.dring[r];
+            diagvL = a.x.diagv[r];
+            barL = a.x.bar[r];
+            dmaxL = a.x.dmax[r];
+        }
 
     Smem sm;
     {
@@ -471,11 +515,15 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const int x = pub_row(k.ph0 + i, c, m, p);
             if (x < 0) continue;
             const size_t so = (size_t)(Q % a.sr) * p + c;
-            a.stW[so] = Wb[(long long)x * w + j];
-            a.stO[so] = Ob[(long long)x * w + j];
+            const double wv0 = Wb[(long long)x * w + j], ov0 = Ob[(long long)x * w + j];
+            QB_COPIES(r) {
+                a.x.stW[r][so] = wv0;
+                a.x.stO[r][so] = ov0;
+            }
             for (int ii = 0; ii < i; ++ii) {
                 const int y = src_row(k.ph0 + ii, x, m);
-                a.stT[((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = (y < p) ? Tb[(long long)y * w + j] : 0.0;
+                const double tv0 = (y < p) ? Tb[(long long)y * w + j] : 0.0;
+                QB_COPIES(r) a.x.stT[r][((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = tv0;
             }
         }
     }
@@ -489,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     }
     __syncthreads();
 
-    unsigned long long* prof = (kProf && a.prof && b == 0) ? a.prof : nullptr;
+    unsigned long long* prof = (kProf && a.prof && bl == 0) ? a.prof : nullptr;
 
     if (warp < kChainWarps) {
         // ================================================================ chain warps
@@ -513,8 +561,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             else bar_chain();
         };
         bar_chain();
-        if (tc == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
-        if (b == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
+        if (tc == 0) qb_arrive(a);
+        if (bl == 0 && tc == 0) a.rec_time[0] = globaltimer_ns();
         double smax = 0.0;  // max |delta| of this thread's own pairs over the sweep
         int snnz = 0;
         long long t_wait = 0, t_load = 0, t_work = 0, t_c0 = 0, t_c3 = 0;
@@ -589,16 +637,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     c = x;
                 }
                 const int cs = c / w;  // slab of column c
-                const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
+                const double* Tc = a.Tfull + (long long)cs * a.slab + (c - cs * w);
                 const size_t so = (size_t)L.slot[d] * p + c;
-                double val = __ldcg(a.stW + so);
-                const double om = __ldcg(a.stO + so);
+                double val = __ldcg(stWL + so);
+                const double om = __ldcg(stOL + so);
                 // in-block phases ph0 .. ph0+d-1: T entries staged by the slab owner; the row's
                 // pair index (into sd) stepped without division
                 double tin[kDMax - 1];
 #pragma unroll
                 for (int i = 0; i < kDMax - 1; ++i)
-                    tin[i] = ldcg_if(a.stT + ((size_t)L.slot[d] * (kDMax - 1) + i) * p + c, i < d);
+                    tin[i] = ldcg_if(stTL + ((size_t)L.slot[d] * (kDMax - 1) + i) * p + c, i < d);
                 {
                     int pos = (x == 0) ? 0 : 1 + (x - 1 + kB.ph0) % m;
                     for (int i = 0; i < d; ++i) {
@@ -613,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 int slot = L.rd0;
 #pragma unroll
                 for (int u = 0; u < 2 * kDMax; ++u) {
-                    dj[u] = ldcg_if(a.dring + (size_t)slot * p + x, u < na);
+                    dj[u] = ldcg_if(dringL + (size_t)slot * p + x, u < na);
                     slot = (slot + 1 == a.rd) ? 0 : slot + 1;
                 }
                 unsigned mask = 0u;
@@ -646,7 +694,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const long long t0 = PCLK();
             const Blk k = block_at(blk, m, D, NB);
             if (tc == 0) {
-                wait_counter(a.bar, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk, blk, a.hang);
+                wait_counter(barL, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk, blk, a.hang,
+                             a.sys_scope);
                 st_vol(&s_epoch, k.g0);  // deltas and lists of every phase < g0 are visible
                 st_vol(&s_blk, blk);
             }
@@ -657,13 +706,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             if (k.ph0 == 0 && blk > 0) {
                 const int it = k.sweep - 1;
                 const double dmax_all =
-                    __longlong_as_double((long long)__ldcg(a.dmax + (a.it_base + it) % WFORM_DMAX_RING));
+                    __longlong_as_double((long long)__ldcg(dmaxL + (a.it_base + it) % WFORM_DMAX_RING));
                 const bool stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter);
-                if (b == 0 && tc == 0) {
+                if (bl == 0 && tc == 0) {
                     a.rec_delta[it] = dmax_all;
                     a.rec_time[it + 1] = globaltimer_ns();
-                    a.dmax[(a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
                 }
+                if (b == 0 && tc == 0)  // recycle the accumulator of sweep it+2 (last read at sweep it-2)
+                    QB_COPIES(r) a.x.dmax[r][(a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
                 if (stop) {
                     if (tc == 0) {
                         s_iters = it + 1;
@@ -698,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         int slot = L.rdb;
 #pragma unroll
                         for (int u = 0; u < kDMax; ++u) {
-                            dj[h][u] = ldcg_if(a.dring + (size_t)slot * p + max(xs[h], 0), xs[h] >= 0 && u < nbv);
+                            dj[h][u] = ldcg_if(dringL + (size_t)slot * p + max(xs[h], 0), xs[h] >= 0 && u < nbv);
                             slot = (slot + 1 == a.rd) ? 0 : slot + 1;
                         }
                     }
@@ -715,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             const int ci = c0i + h * kChain;
                             const int c = mask[h] ? sm.cC()[cb + ci] : 0;
                             const int cs = c / w;  // slab of column c
-                            const double* Tc = a.T + (long long)cs * a.slab + (c - cs * w);
+                            const double* Tc = a.Tfull + (long long)cs * a.slab + (c - cs * w);
                             PartnerWalk pw(max(xs[h], 0), L.phb, m);
 #pragma unroll
                             for (int u = 0; u < kDMax; ++u) {
@@ -821,8 +871,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             dl = sm.sd()[(size_t)d * a.rmax + (q - L.lo[d])];
                             nv = sm.snv()[d * a.share + (q - q_lo)];
                             const size_t dgo = (size_t)L.rdc[d] * p;
-                            a.dring[dgo + r] = dl;  // 0 when the partner is the phantom (odd p)
-                            if (s < p) a.dring[dgo + s] = dl;
+                            QB_COPIES(cp) {
+                                a.x.dring[cp][dgo + r] = dl;  // 0 when the partner is the phantom (odd p)
+                                if (s < p) a.x.dring[cp][dgo + s] = dl;
+                            }
                             if (dl != 0.0) {
                                 smax = fmax(smax, abs_delta(dl));
                                 ++snnz;
@@ -844,14 +896,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         }
                         if (nz) {
                             const size_t seg_off = ((size_t)L.lsl[d] * nblk + b) * a.share;
-                            a.list_rs[seg_off + at] = make_int2(r, s);
-                            a.list_dn[seg_off + at] = make_double2(dl, nv);
+                            QB_COPIES(cp) {
+                                a.x.list_rs[cp][seg_off + at] = make_int2(r, s);
+                                a.x.list_dn[cp][seg_off + at] = make_double2(dl, nv);
+                            }
                         }
                     }
                     bar_colour();
                     if (gt == 0) {  // the thread that arrives: its own stores are ordered by the release
                         for (int d = 0; d < nbc; ++d) {
-                            a.list_cnt[(size_t)L.lsl[d] * nblk + b] = s_cnt[d];
+                            const int cnt_d = s_cnt[d];
+                            QB_COPIES(cp) a.x.list_cnt[cp][(size_t)L.lsl[d] * nblk + b] = cnt_d;
                             s_cnt[d] = 0;
                         }
                     }
@@ -874,8 +929,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         const double om = sm.cO()[cc];
                         const double nv = diag_from_dot(val, om, TD(x), a.n);
                         const double dl = __dsub_rn(nv, om);
-                        a.dring[dgo + x] = dl;
-                        a.diagv[x] = make_double2(dl, nv);
+                        QB_COPIES(cp) {
+                            a.x.dring[cp][dgo + x] = dl;
+                            a.x.diagv[cp][x] = make_double2(dl, nv);
+                        }
                         dm = fmax(dm, abs_delta(dl));
                     }
                     // this sweep's statistics: off-diagonal (own pairs) and diagonal maxima, non-zero count
@@ -894,8 +951,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             mb = fmax(mb, s_red[0][j]);
                             nbk += s_red[1][j];
                         }
-                        atomicMax(a.dmax + (a.it_base + k.sweep) % WFORM_DMAX_RING,
-                                  (unsigned long long)__double_as_longlong(mb));
+                        QB_COPIES(cp)
+                            atomicMax(a.x.dmax[cp] + (a.it_base + k.sweep) % WFORM_DMAX_RING,
+                                      (unsigned long long)__double_as_longlong(mb));
                         atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + k.sweep), (unsigned long long)nbk);
                     }
                 }
@@ -910,7 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, blk, blk + 2, ld_vol(&s_staged), 0, 0);
                     }
                     t_c3 += PCLK() - tw0;
-                    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.bar) : "memory");
+                    qb_arrive(a);
                 }
             }
             // ---- part A of the next block's cells: the prefetch group, concurrently with the
@@ -1047,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         double dj[8], tj[8];
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            dj[u] = ldcg_if(a.dring + (size_t)rslot * p + x, j0 + u <= Cp);
+                            dj[u] = ldcg_if(dringL + (size_t)rslot * p + x, j0 + u <= Cp);
                             rslot = (rslot + 1 == a.rd) ? 0 : rslot + 1;
                         }
                         unsigned mk = 0u;
@@ -1069,8 +1127,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         }
                     }
                     const size_t so = (size_t)(Q % a.sr) * p + c;
-                    a.stW[so] = val;
-                    a.stO[so] = om;
+                    QB_COPIES(cp) {
+                        a.x.stW[cp][so] = val;
+                        a.x.stO[cp][so] = om;
+                    }
                     // T entries of the block's earlier phases (kb.ph0 .. ph-1), for the chain's in-block
                     // FMAs: all loads first (predicated, back to back), then the stores
                     {
@@ -1084,7 +1144,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         }
 #pragma unroll
                         for (int ii = 0; ii < kDMax - 1; ++ii)
-                            if (ii < i) a.stT[((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = tv[ii];
+                            if (ii < i) QB_COPIES(cp) a.x.stT[cp][((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = tv[ii];
                     }
                 }
                 t_stage += PCLK() - ts;
@@ -1121,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
 
             if (diag) {
                 // ---- dense diagonal step over the own slab (+ objective records)
-                const double2* dd = a.diagv;
+                const double2* dd = diagvL;
                 double q_acc = 0.0, pen_acc = 0.0, log_acc = 0.0;
                 for (int i0 = 0; i0 < p; i0 += kPairCap) {
                     const int iend = min(i0 + kPairCap, p);
@@ -1325,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     }
 #undef TD
     __syncthreads();
-    if (b == 0 && tid == 0) {
+    if (bl == 0 && tid == 0) {
         a.status[0] = s_iters;
         a.status[1] = s_conv;
     }
@@ -1359,7 +1419,8 @@ size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int 
 int qblock_colour_warps(int share, int D) { return qb::colour_warps(share, D); }
 
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
-    const size_t smem = qblock_smem_bytes(args.p, nblk, args.share, args.D, args.tdiag_smem, args.nbuf, args.ring_stages);
+    const size_t smem =
+        qblock_smem_bytes(args.p, args.nblk_tot, args.share, args.D, args.tdiag_smem, args.nbuf, args.ring_stages);
     const void* fn = args.prof ? (const void*)qb::pcd_qblock_kernel<true> : (const void*)qb::pcd_qblock_kernel<false>;
     {
         // raise the kernel's shared-memory limit only when needed: setting a function attribute

@@ -96,28 +96,39 @@ struct WformArgs {
 #ifndef QB_DEFAULT_D
 #define QB_DEFAULT_D 4
 #endif
+// Exchange buffers of the blocked kernel, one copy per shard (like WformCopies): writers store
+// into every copy (local HBM, or a peer GPU's over NVLink), readers read their shard's copy.
+struct QbCopies {
+    double2* diagv[WFORM_MAX_SHARDS];       // [p] (delta, new) of the latest diagonal step
+    double* stW[WFORM_MAX_SHARDS];          // [sr][p] staged cell values (W at the block's stage watermark)
+    double* stO[WFORM_MAX_SHARDS];          // [sr][p] staged Omega of the cells
+    double* stT[WFORM_MAX_SHARDS];          // [sr][QB_DMAX-1][p] staged T entries of the block's earlier phases
+    double* dring[WFORM_MAX_SHARDS];        // [rd][p] per-row delta of each recent phase
+    int2* list_rs[WFORM_MAX_SHARDS];        // [rl][nblk_tot][share]
+    double2* list_dn[WFORM_MAX_SHARDS];
+    int* list_cnt[WFORM_MAX_SHARDS];        // [rl][nblk_tot]
+    unsigned long long* bar[WFORM_MAX_SHARDS];   // grid-barrier arrivals (all CTAs of all shards)
+    unsigned long long* dmax[WFORM_MAX_SHARDS];  // [WFORM_DMAX_RING]
+};
 struct QbArgs {
     int p, m, half, w;
     long long slab;
-    double* W;
-    const double* T;
+    double* W;             // this launch's slabs
+    const double* T;       // this launch's slabs
+    const double* Tfull;   // every slab of T (== T unless a process shard): the cells' T entries
     double* Om;
     const double* tdiag;
     int tdiag_smem;
-    double2* diagv;        // [p] (delta, new) of the latest diagonal step
-    double* stW;           // [sr][p] staged cell values (W at the block's stage watermark)
-    double* stO;           // [sr][p] staged Omega of the cells
-    double* stT;           // [sr][QB_DMAX-1][p] staged T entries of the earlier phases of the cell's block
+    QbCopies x;            // exchange buffers, one copy per shard
+    int G;                 // shards
+    int nblk_loc;          // CTAs per shard
+    int nblk_tot;          // CTAs over all shards
+    int blk0;              // global index of this launch's first CTA
+    int sys_scope;         // 1: shards are separate GPUs (system-scope fences for the peer stores)
     int sr;                // stage slots (phases)
-    double* dring;         // [rd][p] per-row delta of each recent phase
     int rd;
-    int2* list_rs;         // [rl][nblk][share]
-    double2* list_dn;
-    int* list_cnt;         // [rl][nblk]
     int rl;
     int share;
-    unsigned long long* bar;
-    unsigned long long* dmax;  // [WFORM_DMAX_RING]
     unsigned long long bar_base;
     int it_base;
     double n, shrink, delta_tol;
@@ -126,9 +137,9 @@ struct QbArgs {
     int cellcap, rmax;     // shared-memory sizing of the block cells
     int stage_window;      // max phases a stage may be brought forward over
     double* rec_delta;
-    double* rec_obj;       // [max_iter][nblk][3]
+    double* rec_obj;       // [max_iter][launch CTAs][3]
     unsigned long long* rec_time;
-    long long* rec_nnz;
+    long long* rec_nnz;    // this launch's pairs (a process shard's part of the sweep)
     int* status;
     unsigned long long* prof;
     long long* hang;       // [8] mapped host memory: watchdog report (what+1, CTA, block, 4 values)

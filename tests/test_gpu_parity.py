@@ -423,3 +423,29 @@ def test_concurrent_lambda_path_from_data_matrix():
     for a, b in zip(seq, con):
         assert a.iterations == b.iterations
         assert np.array_equal(a.estimate.omega, b.estimate.omega)
+
+
+@pytest.mark.parametrize("sys_scope", ["0", "1"])
+def test_virtual_shards_on_the_blocked_kernel(sys_scope, monkeypatch):
+    """The column-sharded fit runs the temporally blocked kernel too (one cross-shard barrier per
+    D=4 colours; stage, delta ring and lists written into every shard's copy): bitwise equal to
+    the unsharded blocked kernel for G = 2, 4, 8, with GPU-scope and -- forced on one device --
+    the multi-GPU system-scope fences and reductions (the reference's worker-invariance contract,
+    test_solver.py:222-230)."""
+    monkeypatch.setenv("CONCORD_FORCE_SYS_SCOPE", sys_scope)
+    _, t = synth.problem("ar2", 1000, 500, seed=6)
+    g = cb.GramMatrix(t, 500)
+    with cb.Solver(1000) as s1:
+        assert s1.layout()["kernel"] == 4
+        s1.set_gram(g)
+        want = [s1.fit(lam, 1e-5, 500) for lam in (0.3, 0.1)]
+    for G in (2, 4, 8):
+        with cb.Solver(1000, n_shards=G) as sg:
+            lay = sg.layout()
+            assert lay["n_shards"] == G and lay["kernel"] == 4
+            sg.set_gram(g)
+            for lam, w in zip((0.3, 0.1), want):  # consecutive fits: barrier and sweep bases carried
+                r = sg.fit(lam, 1e-5, 500)
+                assert r.iterations == w.iterations and r.edge_count == w.edge_count
+                assert np.array_equal(r.estimate.omega, w.estimate.omega)
+                np.testing.assert_allclose(r.objective_trace, w.objective_trace, rtol=1e-12)
