@@ -1,16 +1,21 @@
 """Multi-GPU CONCORD-PCD: one process per GPU, column-sharded.
 
 W = Omega*T, T and Omega are split by column block: GPU g owns slabs
-[g*B, (g+1)*B) of the kernel's column slabs (B = blocks per shard).  A colour
-step needs, in every CTA of every GPU, the published half values W[x,c] of
-all p columns, so the only data-path exchange is an all-gather of p
-(W, Omega) pairs per colour (plus the per-row deltas and the non-zero delta
-lists).  It happens INSIDE the persistent kernel: each CTA stores its values
-into every GPU's copy of the exchange buffers through NVLink peer pointers
-(cudaIpc handles opened here) and arrives on every GPU's barrier counter; no
-host NCCL call per colour.  Every GPU evaluates identical arithmetic, so the
-estimate is bitwise identical for any GPU count -- the analogue of the
-reference's worker invariance (test_solver.py:222-230).
+[g*B, (g+1)*B) of the kernel's column slabs (B = blocks per shard).  The
+fit runs the temporally blocked kernel (csrc/pcd_qblock.cu) on every GPU:
+each CTA owns a range of pair indices and evaluates D=4 colours per grid
+barrier, so the cross-GPU barrier is paid once per 4 colours.  Its data-path
+exchange is the cells the colours read -- the slab owners' staged (W, Omega,
+T) entries -- plus the per-row delta ring, the non-zero delta lists and the
+diagonal step's (delta, new) vector.  It happens INSIDE the persistent
+kernel: each writer stores into every GPU's copy of these buffers through
+NVLink peer pointers (cudaIpc handles of one arena per GPU, opened here),
+fences at system scope and arrives on every GPU's barrier counter; no host
+NCCL call per colour.  T is replicated (the cells read T entries of every
+column).  Every GPU evaluates identical arithmetic, so the estimate is
+bitwise identical for any GPU count -- the analogue of the reference's
+worker invariance (test_solver.py:222-230).  p < 256 uses the per-phase
+kernel (csrc/pcd_wform.cu) with the same exchange per colour.
 
 torch.distributed is the plumbing only: it all-gathers the 64-byte IPC
 handles once, and at the end all-reduces the per-sweep objective partials /
