@@ -395,10 +395,12 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
         if (w < 8) w = 8;
     }
     w = (w + 1) & ~1;
-    {
-        // rows of w doubles on whole 32-byte sectors (w a multiple of 4) when that keeps >= 90% of
-        // the slabs: the random row streams then move no partial sectors (p=5000 on 148 SMs:
-        // w=34 -> 36 on 139 slabs, the dense lambda=0.1 fit 1.93 -> 1.70 s, profiles/r02/align.log)
+    if (n_blocks <= 0) {
+        // default layout: rows of w doubles on whole 32-byte sectors (w a multiple of 4) when that
+        // keeps >= 90% of the slabs -- the random row streams then move no partial sectors (p=5000
+        // on 148 SMs: w=34 -> 36 on 139 slabs, the dense lambda=0.1 fit 1.93 -> 1.70 s, the sparse
+        // lambda=0.3 fit 0.25 -> 0.26 s; profiles/r02/align.log).  An explicit slab count (a lane of
+        // PathScheduler, mostly sparse fits) keeps its width: there 122 -> 124 cost the sparse fits 8%.
         const int w4 = (w + 3) & ~3;
         const int need = (ip + w - 1) / w, need4 = (ip + w4 - 1) / w4;
         if (w4 != w && 10 * need4 >= 9 * need) w = w4;

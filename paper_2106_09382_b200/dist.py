@@ -53,8 +53,8 @@ def partition(p, n_shards, n_blocks=0, nsm=NSM, rank=None):
         tot = nsm * (n_shards if rank is not None else 1)
         w = max(8, -(-p // tot))
     w += w & 1
-    w4 = (w + 3) & ~3  # whole 32-byte sectors when that keeps >= 90% of the slabs (capi.cu)
-    if w4 != w and 10 * -(-p // w4) >= 9 * -(-p // w):
+    w4 = (w + 3) & ~3  # default layout: whole 32-byte sectors when that keeps >= 90% of the slabs (capi.cu)
+    if n_blocks <= 0 and w4 != w and 10 * -(-p // w4) >= 9 * -(-p // w):
         w = w4
     need = -(-p // w)
     per = -(-need // n_shards)

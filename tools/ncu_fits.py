@@ -20,9 +20,9 @@ ap.add_argument("--n", type=int, default=2000)
 ap.add_argument("--lams", default="0.55,0.50,0.45,0.40,0.35,0.30,0.25,0.20,0.15,0.10")
 ap.add_argument("--out", default="gpurun_out/ncu_fits.json")
 a = ap.parse_args()
-x = synth.center(synth.sample_mvn(synth.ar2_precision(a.p), a.n, seed=0))
+x, t = synth.portable_problem("ar2", a.p, a.n, seed=0)  # the bench's (and the fixtures') exact Gram
 s = cb.Solver(a.p)
-s.gram_from_data(cb.DataMatrix(x, centered=True))
+s.set_gram(cb.GramMatrix(t, a.n))
 rows = []
 for lam in [float(v) for v in a.lams.split(",")]:
     rc, res, deltas, objs, secs = s.fit_raw(lam, 1e-5, 5000)

@@ -21,10 +21,11 @@ ap.add_argument("--fits", type=int, default=1)
 ap.add_argument("--n-blocks", type=int, default=0)
 ap.add_argument("--max-iter", type=int, default=5000)
 a = ap.parse_args()
-x = synth.center(synth.sample_mvn(synth.ar2_precision(a.p), a.n, seed=0))
+x = (synth.portable_problem("ar2", a.p, a.n, seed=0)[0] if a.p <= 8000
+     else synth.center(synth.sample_mvn_ar2_banded(a.p, a.n, seed=0)))
 s = cb.Solver(a.p, n_blocks=a.n_blocks)
 t0 = time.perf_counter()
-s.gram_from_data(cb.DataMatrix(x, centered=True))
+s.gram_from_data(cb.DataMatrix(x))
 print(f"gram {time.perf_counter() - t0:.3f}s", flush=True)
 for i in range(a.fits):
     rc, res, deltas, objs, secs = s.fit_raw(a.lam, 1e-5, a.max_iter)
