@@ -132,6 +132,11 @@ struct concord_solver {
     int qb_D = 0, qb_NB = 0, qb_sr = 0, qb_rd = 0, qb_rl = 0;
     int qb_nbuf = 1, qb_td = 0, qb_ring = 6;  // shared-memory plan of the blocked kernel
     double* Tfull = nullptr;  // process shard on the blocked kernel: every slab of T (the cells' T entries)
+    // storage of W, T, Om: local slab b, row i, slab column j at b * ss + i * ld + j.  Row-major
+    // (ss = w, ld = the launch's columns) for the blocked kernel -- every CTA streams the same
+    // rows at the same time, so each row is one contiguous DRAM stretch; slab layout (ss = p*w,
+    // ld = w) for the per-phase kernel.  ssT / ldT: the same for Tfull.
+    long long ss = 0, ld = 0, ssT = 0, ldT = 0;
     long long* hang = nullptr;  // mapped host memory: the fit kernels' watchdog report
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -205,8 +210,9 @@ int set_gram_rowmajor(concord_solver* s, const double* src, int32_t where) {
                            s->stream));
         dsrc = s->stage;
     }
-    CK(launch_pack_slabs(dsrc, s->p, s->T, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
-    if (s->Tfull) CK(launch_pack_slabs(dsrc, s->p, s->Tfull, s->p, s->w, s->nblk_tot, 0, s->stream));
+    CK(launch_pack_slabs(dsrc, s->p, s->T, s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->stream));
+    if (s->Tfull)
+        CK(launch_pack_slabs(dsrc, s->p, s->Tfull, s->p, s->w, s->ssT, s->ldT, s->nblk_tot, 0, s->stream));
     CK(launch_rowmajor_diag(dsrc, s->tdiag, s->p, s->stream));
     std::vector<double> d(s->p);
     CK(cudaMemcpyAsync(d.data(), s->tdiag, sizeof(double) * s->p, cudaMemcpyDeviceToHost, s->stream));
@@ -222,13 +228,13 @@ int set_gram_rowmajor(concord_solver* s, const double* src, int32_t where) {
 
 int download_slabs(concord_solver* s, const double* src, double* out, int32_t where) {
     if (where == CONCORD_DEVICE) {
-        CK(launch_unpack_slabs(src, out, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
+        CK(launch_unpack_slabs(src, out, s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->stream));
         CK(cudaStreamSynchronize(s->stream));
         return CONCORD_OK;
     }
     int rc = ensure_stage(s);
     if (rc) return rc;
-    CK(launch_unpack_slabs(src, s->stage, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
+    CK(launch_unpack_slabs(src, s->stage, s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->stream));
     CK(cudaMemcpyAsync(out, s->stage, sizeof(double) * (size_t)s->p * ncols_local(s), cudaMemcpyDeviceToHost,
                        s->stream));
     CK(cudaStreamSynchronize(s->stream));
@@ -277,8 +283,8 @@ int init_warm(concord_solver* s, const double* om, int32_t where) {
     int rc = ensure_stage(s);
     if (rc) return rc;
     CK(cudaMemcpyAsync(s->stage, h, sizeof(double) * (size_t)p * p, cudaMemcpyHostToDevice, s->stream));
-    CK(launch_pack_slabs(s->stage, p, s->Om, p, s->w, s->nblk_launch, s->blk0, s->stream));
-    CK(launch_wform_init_csr(s->csr_rowptr, s->csr_col, s->csr_val, s->T, s->W, p, s->w, s->nblk_launch,
+    CK(launch_pack_slabs(s->stage, p, s->Om, p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->stream));
+    CK(launch_wform_init_csr(s->csr_rowptr, s->csr_col, s->csr_val, s->T, s->W, p, s->w, s->ss, s->ld, s->nblk_launch,
                              s->stream));
     CK(cudaStreamSynchronize(s->stream));  // host vectors go out of scope
     return CONCORD_OK;
@@ -474,6 +480,13 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
         }
         s->L = s->qb ? arena_layout(ip, s->rd, s->rl, s->nblk_tot, s->share, s->qb_sr, s->qb_rd, s->qb_rl)
                      : arena_layout(ip, s->rd, s->rl, s->nblk_tot, s->share);
+        // row-major storage for the blocked kernel (32-bit double2 row offsets: p * columns / 2 < 2^31)
+        bool rowmajor = s->qb && (long long)ip * s->nblk_tot * w / 2 < (1LL << 31);
+        if (const char* e = getenv("CONCORD_LAYOUT")) rowmajor = rowmajor && strcmp(e, "slab") != 0;
+        s->ss = rowmajor ? w : s->slab;
+        s->ld = rowmajor ? (long long)s->nblk_launch * w : w;
+        s->ssT = rowmajor ? w : s->slab;
+        s->ldT = rowmajor ? (long long)s->nblk_tot * w : w;
     }
     for (int r = 0; r < G; ++r) {
         if (rank >= 0 && r != rank) continue;  // peers' arenas are opened by concord_shard_open_peers
@@ -684,7 +697,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         rc = init_warm(s, prm->omega_init, prm->init_where);
         if (rc) return rc;
     } else {
-        CK(launch_slab_identity(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->stream));
+        CK(launch_slab_identity(s->Om, s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->stream));
         CK(cudaMemcpyAsync(s->W, s->T, sizeof(double) * tot, cudaMemcpyDeviceToDevice, s->stream));
     }
     CK(cudaMemsetAsync(s->rec_nnz, 0, sizeof(long long) * prm->max_iter, s->stream));
@@ -747,7 +760,10 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.m = a.m;
         q.half = a.half;
         q.w = a.w;
-        q.slab = a.slab;
+        q.slab = s->ss;
+        q.ld = (int)s->ld;
+        q.slabT = s->Tfull ? s->ssT : s->ss;
+        q.ldT = (int)(s->Tfull ? s->ldT : s->ld);
         q.W = a.W;
         q.T = a.T;
         q.Tfull = s->Tfull ? s->Tfull : a.T;
@@ -804,7 +820,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
     }
     CK(cudaEventRecord(s->ev[2], s->stream));
-    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->edges, s->stream));
+    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->edges, s->stream));
 
     int status[2] = {0, 0};
     unsigned long long edges = 0;
@@ -952,7 +968,7 @@ int concord_solver_edge_count(concord_solver* s, int64_t* out) {
     if (!s || !out) return fail(CONCORD_ERR_ARG, "NULL argument");
     DeviceGuard g(s->dev);
     unsigned long long edges = 0;
-    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->nblk_launch, s->blk0, s->edges, s->stream));
+    CK(launch_slab_edge_count(s->Om, s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->edges, s->stream));
     CK(cudaMemcpyAsync(&edges, s->edges, sizeof(edges), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     *out = (int64_t)edges;
@@ -983,7 +999,7 @@ int concord_solver_check_optimality(concord_solver* s, double lam, double* worst
     cudaError_t e = dalloc(&bi, nb);
     std::vector<double> hv(nb);
     std::vector<long long> hi(nb);
-    if (e == cudaSuccess) e = launch_optimality(s->W, s->Om, s->p, s->w, s->n, s->n * lam, bv, bi, nb, s->stream);
+    if (e == cudaSuccess) e = launch_optimality(s->W, s->Om, s->p, s->w, s->ss, s->ld, s->n, s->n * lam, bv, bi, nb, s->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hv.data(), bv, sizeof(double) * nb, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hi.data(), bi, sizeof(long long) * nb, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
@@ -1012,7 +1028,7 @@ int concord_solver_estimate_entries(concord_solver* s, int64_t* count, int32_t* 
     int* rowcnt = nullptr;
     CK(dalloc(&rowcnt, p));
     std::vector<int> hc(p);
-    cudaError_t e = launch_triplet_count(s->Om, p, s->w, rowcnt, s->stream);
+    cudaError_t e = launch_triplet_count(s->Om, p, s->w, s->ss, s->ld, rowcnt, s->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), rowcnt, sizeof(int) * p, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     cudaFree(rowcnt);
@@ -1030,7 +1046,7 @@ int concord_solver_estimate_entries(concord_solver* s, int64_t* count, int32_t* 
     if (e == cudaSuccess) e = dalloc(&dj, off[p]);
     if (e == cudaSuccess) e = dalloc(&dv, off[p]);
     if (e == cudaSuccess) e = cudaMemcpyAsync(doff, off.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s->stream);
-    if (e == cudaSuccess) e = launch_triplet_write(s->Om, p, s->w, doff, di, dj, dv, s->stream);
+    if (e == cudaSuccess) e = launch_triplet_write(s->Om, p, s->w, s->ss, s->ld, doff, di, dj, dv, s->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(ii, di, sizeof(int) * off[p], cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(jj, dj, sizeof(int) * off[p], cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(vv, dv, sizeof(double) * off[p], cudaMemcpyDeviceToHost, s->stream);

@@ -19,13 +19,14 @@
 
 namespace concord {
 
-__device__ __forceinline__ double slab_at(const double* slab, int p, int w, int i, int j) {
+__device__ __forceinline__ double slab_at(const double* slab, int w, long long ss, long long rs, int i, int j) {
     const int b = j / w;
-    return slab[(long long)b * p * w + (long long)i * w + (j - b * w)];
+    return slab[(long long)b * ss + (long long)i * rs + (j - b * w)];
 }
 
 // Per-thread worst (value, flat index) over the upper triangle, reduced per block.
 __global__ void optimality_kernel(const double* __restrict__ W, const double* __restrict__ Om, int p, int w,
+                                  long long ss, long long rs,
                                   double n, double weight, double* __restrict__ blk_val,
                                   long long* __restrict__ blk_idx) {
     double best = -1.0;
@@ -35,12 +36,12 @@ __global__ void optimality_kernel(const double* __restrict__ W, const double* __
          e += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(e / p), j = (int)(e - (long long)i * p);
         if (j < i) continue;
-        const double om = slab_at(Om, p, w, i, j);
+        const double om = slab_at(Om, w, ss, rs, i, j);
         double v;
         if (i == j) {
-            v = fabs(slab_at(W, p, w, i, i) - n / om);
+            v = fabs(slab_at(W, w, ss, rs, i, i) - n / om);
         } else {
-            const double g = slab_at(W, p, w, i, j) + slab_at(W, p, w, j, i);
+            const double g = slab_at(W, w, ss, rs, i, j) + slab_at(W, w, ss, rs, j, i);
             v = (om != 0.0) ? fabs(g + weight * (om > 0.0 ? 1.0 : -1.0)) : fmax(fabs(g) - weight, 0.0);
         }
         if (v > best || (v == best && e < bidx)) {
@@ -78,10 +79,11 @@ __global__ void optimality_kernel(const double* __restrict__ W, const double* __
 }
 
 // Entries row i stores: j = i, and j > i with omega_ij != 0.
-__global__ void triplet_count_kernel(const double* __restrict__ Om, int p, int w, int* __restrict__ rowcnt) {
+__global__ void triplet_count_kernel(const double* __restrict__ Om, int p, int w, long long ss, long long rs,
+                                     int* __restrict__ rowcnt) {
     for (int i = blockIdx.x; i < p; i += gridDim.x) {
         int c = 0;
-        for (int j = i + 1 + threadIdx.x; j < p; j += blockDim.x) c += slab_at(Om, p, w, i, j) != 0.0;
+        for (int j = i + 1 + threadIdx.x; j < p; j += blockDim.x) c += slab_at(Om, w, ss, rs, i, j) != 0.0;
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         __shared__ int sc[32];
         if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = c;
@@ -96,7 +98,8 @@ __global__ void triplet_count_kernel(const double* __restrict__ Om, int p, int w
 }
 
 // Row i writes its entries in ascending j at rowoff[i] (exclusive scan of rowcnt).
-__global__ void triplet_write_kernel(const double* __restrict__ Om, int p, int w, const long long* __restrict__ rowoff,
+__global__ void triplet_write_kernel(const double* __restrict__ Om, int p, int w, long long ss, long long rs,
+                                     const long long* __restrict__ rowoff,
                                      int* __restrict__ ti, int* __restrict__ tj, double* __restrict__ tv) {
     __shared__ int s_base;
     __shared__ int sc[32];
@@ -105,14 +108,14 @@ __global__ void triplet_write_kernel(const double* __restrict__ Om, int p, int w
         if (threadIdx.x == 0) {
             ti[at] = i;
             tj[at] = i;
-            tv[at] = slab_at(Om, p, w, i, i);
+            tv[at] = slab_at(Om, w, ss, rs, i, i);
             s_base = 0;
         }
         ++at;
         __syncthreads();
         for (int j0 = i + 1; j0 < p; j0 += blockDim.x) {
             const int j = j0 + threadIdx.x;
-            const double v = (j < p) ? slab_at(Om, p, w, i, j) : 0.0;
+            const double v = (j < p) ? slab_at(Om, w, ss, rs, i, j) : 0.0;
             const bool nz = v != 0.0;
             const unsigned mask = __ballot_sync(0xffffffffu, nz);
             const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -136,20 +139,23 @@ __global__ void triplet_write_kernel(const double* __restrict__ Om, int p, int w
     }
 }
 
-cudaError_t launch_optimality(const double* W, const double* Om, int p, int w, double n, double weight,
+cudaError_t launch_optimality(const double* W, const double* Om, int p, int w, long long ss, long long rs, double n,
+                              double weight,
                               double* blk_val, long long* blk_idx, int nblocks, cudaStream_t st) {
-    optimality_kernel<<<nblocks, 256, 0, st>>>(W, Om, p, w, n, weight, blk_val, blk_idx);
+    optimality_kernel<<<nblocks, 256, 0, st>>>(W, Om, p, w, ss, rs, n, weight, blk_val, blk_idx);
     return cudaGetLastError();
 }
 
-cudaError_t launch_triplet_count(const double* Om, int p, int w, int* rowcnt, cudaStream_t st) {
-    triplet_count_kernel<<<p < 148 * 8 ? p : 148 * 8, 256, 0, st>>>(Om, p, w, rowcnt);
+cudaError_t launch_triplet_count(const double* Om, int p, int w, long long ss, long long rs, int* rowcnt,
+                                 cudaStream_t st) {
+    triplet_count_kernel<<<p < 148 * 8 ? p : 148 * 8, 256, 0, st>>>(Om, p, w, ss, rs, rowcnt);
     return cudaGetLastError();
 }
 
-cudaError_t launch_triplet_write(const double* Om, int p, int w, const long long* rowoff, int* ti, int* tj,
+cudaError_t launch_triplet_write(const double* Om, int p, int w, long long ss, long long rs, const long long* rowoff,
+                                 int* ti, int* tj,
                                  double* tv, cudaStream_t st) {
-    triplet_write_kernel<<<p < 148 * 8 ? p : 148 * 8, 256, 0, st>>>(Om, p, w, rowoff, ti, tj, tv);
+    triplet_write_kernel<<<p < 148 * 8 ? p : 148 * 8, 256, 0, st>>>(Om, p, w, ss, rs, rowoff, ti, tj, tv);
     return cudaGetLastError();
 }
 

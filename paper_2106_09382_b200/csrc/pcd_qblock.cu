@@ -183,7 +183,7 @@ __device__ int apply_scan(int* s, int n, int ta, int* s_wsum) {
 // registers allow. Each thread only reads the
 // slots it filled, so no barrier is needed; cp.async.wait_group orders them.
 __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double* L_d, const int* L_ph, int only,
-                                                 int e_lo, int e_hi, int w2, double* __restrict__ Wb,
+                                                 int e_lo, int e_hi, int w2, long long ld2, double* __restrict__ Wb,
                                                  const double* __restrict__ Tb, double2* ring, int ta, int S) {
     const int per = 2 * w2;
     const int items = (e_hi - e_lo) * per;
@@ -206,8 +206,8 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
         const int h = c.rem >= w2;
         const int j2 = c.rem - h * w2;
         const int2 rs = L_rs[e];
-        off_w = (h ? rs.y : rs.x) * w2 + j2;
-        off_t = (h ? rs.x : rs.y) * w2 + j2;
+        off_w = (h ? rs.y : rs.x) * ld2 + j2;
+        off_t = (h ? rs.x : rs.y) * ld2 + j2;
     };
     Cursor ci{ta / per, ta - (ta / per) * per};  // next item to issue
     Cursor cc = ci;                               // next item to complete
@@ -269,7 +269,7 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
 // phase order -- the same operations, in the same order, as phase-by-phase passes, in one
 // round trip instead of one per phase.
 __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d, const int* L_ph, int nent, int w2,
-                                             double* __restrict__ Wb, const double* __restrict__ Tb, short* s_next,
+                                             int ld2, double* __restrict__ Wb, const double* __restrict__ Tb, short* s_next,
                                              unsigned char* s_first, int ta) {
     for (int he = ta; he < 2 * nent; he += kApply) {
         const int e = he >> 1;
@@ -300,7 +300,7 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
         const int j2 = idx - he * w2;
         const int2 rs0 = L_rs[he >> 1];
         const int dst = (he & 1) ? rs0.y : rs0.x;
-        double2* wp = reinterpret_cast<double2*>(Wb) + (long long)dst * w2 + j2;
+        double2* wp = reinterpret_cast<double2*>(Wb) + (long long)dst * ld2 + j2;
         double2 wv = __ldcg(wp);
         // the chain, four links at a time: T loads of a group back to back, then its FMAs
         int k = he;
@@ -321,7 +321,7 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
             double2 tv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (u < len) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb) + (long long)srcs[u] * w2 + j2);
+                if (u < len) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb) + (long long)srcs[u] * ld2 + j2);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (u < len) {
@@ -334,9 +334,12 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
 }
 
 #define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) \
-    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_, a.ring_stages)
+    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, ld2, Wb_, Tb_, ring_, ta_, a.ring_stages)
 
-#define QB_COPIES(r) _Pragma("unroll") for (int r = 0; r < WFORM_MAX_SHARDS; ++r) if (r < a.G)
+#define QB_COPIES_RT(r) _Pragma("unroll") for (int r = 0; r < WFORM_MAX_SHARDS; ++r) if (r < a.G)
+// In the kernel: one copy unless the launch is sharded (kShard), so the unsharded instance carries
+// no per-copy predicates in its store loops.
+#define QB_COPIES(r) _Pragma("unroll") for (int r = 0; r < (kShard ? WFORM_MAX_SHARDS : 1); ++r) if (!kShard || r < a.G)
 
 // Arrive on the grid barrier of every shard: this CTA's exchange-buffer stores (its own and, through
 // the CTA barrier before the call, its other threads') become visible at GPU scope -- or system
@@ -345,12 +348,12 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
 __device__ __forceinline__ void qb_arrive(const QbArgs& a) {
     if (a.sys_scope) {
         asm volatile("fence.acq_rel.sys;" ::: "memory");
-        QB_COPIES(r) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
+        QB_COPIES_RT(r) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
     } else if (a.G == 1) {
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[0]) : "memory");
     } else {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        QB_COPIES(r) asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
+        QB_COPIES_RT(r) asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(a.x.bar[r]) : "memory");
     }
 }
 
@@ -421,7 +424,7 @@ struct Smem {
 
 // kProf: the phase profiler (CONCORD_PHASE_PROFILE); the production instantiation carries
 // no timers at all (they would hold ~30 registers across the loops).
-template <bool kProf>
+template <bool kProf, bool kShard>
 #define PCLK() (kProf ? clock64() : 0ll)
 __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     __shared__ int s_epoch, s_blk, s_stop, s_staged, s_iters, s_conv;
@@ -444,6 +447,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     const int c0 = b * w;
     const int wl = max(0, min(w, p - c0));
     const int q_lo = min(b * a.share, half), q_hi = min(q_lo + a.share, half);
+    // slab bl of this launch: element (row x, column c0 + j) at base + bl * a.slab + x * ld + j
+    // (row-major layout: a.slab = w, ld = the launch's columns; slab layout: a.slab = p * w, ld = w)
+    const int ld = a.ld, ld2 = a.ld >> 1;
     double* __restrict__ Wb = a.W + (long long)bl * a.slab;
     const double* __restrict__ Tb = a.T + (long long)bl * a.slab;
     double* __restrict__ Ob = a.Om + (long long)bl * a.slab;
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
     const unsigned long long* barL = a.x.bar[0];
     const unsigned long long* dmaxL = a.x.dmax[0];
 #pragma unroll
-    for (int r = 1; r < WFORM_MAX_SHARDS; ++r)
+    for (int r = 1; r < (kShard ? WFORM_MAX_SHARDS : 1); ++r)
         if (r == shard) {
             lcntL = a.x.list_cnt[r];
             lrsL = a.x.list_rs[r];
@@ -515,14 +521,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             const int x = pub_row(k.ph0 + i, c, m, p);
             if (x < 0) continue;
             const size_t so = (size_t)(Q % a.sr) * p + c;
-            const double wv0 = Wb[(long long)x * w + j], ov0 = Ob[(long long)x * w + j];
+            const double wv0 = Wb[(long long)x * ld + j], ov0 = Ob[(long long)x * ld + j];
             QB_COPIES(r) {
                 a.x.stW[r][so] = wv0;
                 a.x.stO[r][so] = ov0;
             }
             for (int ii = 0; ii < i; ++ii) {
                 const int y = src_row(k.ph0 + ii, x, m);
-                const double tv0 = (y < p) ? Tb[(long long)y * w + j] : 0.0;
+                const double tv0 = (y < p) ? Tb[(long long)y * ld + j] : 0.0;
                 QB_COPIES(r) a.x.stT[r][((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = tv0;
             }
         }
@@ -637,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     c = x;
                 }
                 const int cs = c / w;  // slab of column c
-                const double* Tc = a.Tfull + (long long)cs * a.slab + (c - cs * w);
+                const double* Tc = a.Tfull + (long long)cs * a.slabT + (c - cs * w);
                 const size_t so = (size_t)L.slot[d] * p + c;
                 double val = __ldcg(stWL + so);
                 const double om = __ldcg(stOL + so);
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     PartnerWalk pw(x, L.ph0w, m);
 #pragma unroll
                     for (int u = 0; u < 2 * kDMax; ++u) {
-                        tj[u] = ldcg_if(Tc + (long long)pw.y() * w, (mask >> u) & 1u);
+                        tj[u] = ldcg_if(Tc + (long long)pw.y() * a.ldT, (mask >> u) & 1u);
                         pw.next();
                     }
 #pragma unroll
@@ -765,11 +771,11 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             const int ci = c0i + h * kChain;
                             const int c = mask[h] ? sm.cC()[cb + ci] : 0;
                             const int cs = c / w;  // slab of column c
-                            const double* Tc = a.Tfull + (long long)cs * a.slab + (c - cs * w);
+                            const double* Tc = a.Tfull + (long long)cs * a.slabT + (c - cs * w);
                             PartnerWalk pw(max(xs[h], 0), L.phb, m);
 #pragma unroll
                             for (int u = 0; u < kDMax; ++u) {
-                                tj[h][u] = ldcg_if(Tc + (long long)pw.y() * w, (mask[h] >> u) & 1u);
+                                tj[h][u] = ldcg_if(Tc + (long long)pw.y() * a.ldT, (mask[h] >> u) & 1u);
                                 pw.next();
                             }
                         }
@@ -1095,8 +1101,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const int c = c0 + j;
                     const int x = pub_row(kb.ph0 + i, c, m, p);
                     if (x < 0) continue;
-                    double val = __ldcg(Wb + (long long)x * w + j);
-                    const double om = __ldcg(Ob + (long long)x * w + j);
+                    double val = __ldcg(Wb + (long long)x * ld + j);
+                    const double om = __ldcg(Ob + (long long)x * ld + j);
                     // deltas of phases C+1 .. Cp, eight at a time: ring loads back to back, then the
                     // T entries of the phases that moved row x (predicated, back to back), then the FMAs
                     int rslot = (C + 1) % a.rd;
@@ -1115,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         if (mk) {
 #pragma unroll
                             for (int u = 0; u < 8; ++u) {
-                                tj[u] = ldcg_if(Tb + (long long)pw.y() * w + j, (mk >> u) & 1u);
+                                tj[u] = ldcg_if(Tb + (long long)pw.y() * ld + j, (mk >> u) & 1u);
                                 pw.next();
                             }
 #pragma unroll
@@ -1139,7 +1145,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
 #pragma unroll
                         for (int ii = 0; ii < kDMax - 1; ++ii) {
                             const int y = pt.y();
-                            tv[ii] = ldcg_if(Tb + (long long)min(y, p - 1) * w + j, ii < i && y < p);
+                            tv[ii] = ldcg_if(Tb + (long long)min(y, p - 1) * ld + j, ii < i && y < p);
                             pt.next();
                         }
 #pragma unroll
@@ -1165,8 +1171,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     } else {
                         s_multi = 1;
                     }
-                    if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
-                    if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                    if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * ld + (rs.y - c0)] = dn.y;
+                    if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * ld + (rs.x - c0)] = dn.y;
                 }
             }
             bar_apply();
@@ -1200,7 +1206,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             if (idx < items) {
                                 const int ii = idx / w2;
                                 const int j2 = idx - ii * w2;
-                                const long long off = (long long)(i0 + ii) * w + 2 * j2;
+                                const long long off = (long long)(i0 + ii) * ld + 2 * j2;
                                 wv[u] = __ldcg(reinterpret_cast<const double2*>(Wb + off));
                                 if (sm.L_d()[ii] != 0.0) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + off));
                                 if (a.want_trace) ov[u] = *reinterpret_cast<const double2*>(Ob + off);
@@ -1213,7 +1219,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 const int ii = idx / w2;
                                 const int j2 = idx - ii * w2;
                                 const int i = i0 + ii;
-                                const long long off = (long long)i * w + 2 * j2;
+                                const long long off = (long long)i * ld + 2 * j2;
                                 const double d = sm.L_d()[ii];
                                 if (d != 0.0) {
                                     wv[u].x = fma(d, tv[u].x, wv[u].x);
@@ -1290,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if (!s_conflict) {
                         ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, 0, nent, w2, Wb, Tb, sm.ring(), ta);
                     } else if (nent <= kChainN) {
-                        apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), nent, w2, Wb, Tb, s_next, s_first, ta);
+                        apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), nent, w2, ld2, Wb, Tb, s_next, s_first, ta);
                     } else {
                         for (int jb = 0; jb < nb; ++jb) {  // rows repeat across phases: phase by phase
                             ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), jb, 0, nent, w2, Wb, Tb, sm.ring(), ta);
@@ -1326,8 +1332,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             const double2 dn = __ldcg(ldnL + at);
                             // segments with one entry had their Omega cells written above
                             if (sm.s_off()[lo + 1] - sm.s_off()[lo] > 1) {
-                                if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * w + (rs.y - c0)] = dn.y;
-                                if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * w + (rs.x - c0)] = dn.y;
+                                if ((unsigned)(rs.y - c0) < (unsigned)wl) Ob[(long long)rs.x * ld + (rs.y - c0)] = dn.y;
+                                if ((unsigned)(rs.x - c0) < (unsigned)wl) Ob[(long long)rs.y * ld + (rs.x - c0)] = dn.y;
                             }
                             sm.L_rs()[e - e0] = rs;
                             sm.L_d()[e - e0] = dn.x;
@@ -1421,14 +1427,18 @@ int qblock_colour_warps(int share, int D) { return qb::colour_warps(share, D); }
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
     const size_t smem =
         qblock_smem_bytes(args.p, args.nblk_tot, args.share, args.D, args.tdiag_smem, args.nbuf, args.ring_stages);
-    const void* fn = args.prof ? (const void*)qb::pcd_qblock_kernel<true> : (const void*)qb::pcd_qblock_kernel<false>;
+    const bool shard = args.G > 1;
+    const void* fn = args.prof ? (shard ? (const void*)qb::pcd_qblock_kernel<true, true>
+                                        : (const void*)qb::pcd_qblock_kernel<true, false>)
+                               : (shard ? (const void*)qb::pcd_qblock_kernel<false, true>
+                                        : (const void*)qb::pcd_qblock_kernel<false, false>);
     {
         // raise the kernel's shared-memory limit only when needed: setting a function attribute
         // while another fit runs the kernel on another stream serialises the two
         static std::mutex mu;
-        static size_t set_bytes[2] = {0, 0};
+        static size_t set_bytes[4] = {0, 0, 0, 0};
         std::lock_guard<std::mutex> lock(mu);
-        size_t& cur = set_bytes[args.prof ? 1 : 0];
+        size_t& cur = set_bytes[(args.prof ? 2 : 0) + (shard ? 1 : 0)];
         if (smem > cur) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;

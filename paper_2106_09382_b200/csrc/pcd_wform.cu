@@ -894,10 +894,13 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_wform_kernel(WformArgs a) {
 
 
 // --------------------------------------------------------------- layout kernels
+// Slab storage: local slab b (global column block blk0 + b), row i, column j of the slab at
+// b * ss + i * rs + j -- slab layout ss = p*w, rs = w; row-major layout ss = w, rs = nblk*w.
+
 // Row-major p x p (leading dim ld) -> nblk slabs of width w starting at global
 // column block blk0 (zero padding past column p).
 __global__ void pack_slabs_kernel(const double* __restrict__ src, long long ld, double* __restrict__ dst,
-                                  int p, int w, int nblk, int blk0) {
+                                  int p, int w, long long ss, long long rs, int nblk, int blk0) {
     const long long total = (long long)nblk * p * w;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
@@ -906,20 +909,20 @@ __global__ void pack_slabs_kernel(const double* __restrict__ src, long long ld, 
         const int i = (int)(rem / w);
         const int j = (int)(rem - (long long)i * w);
         const long long c = (blk0 + b) * w + j;
-        dst[e] = (c < p) ? src[(long long)i * ld + c] : 0.0;
+        dst[b * ss + (long long)i * rs + j] = (c < p) ? src[(long long)i * ld + c] : 0.0;
     }
 }
 
 // Slabs -> row-major p x ncols (ncols = columns the slabs hold, clipped to p).
 __global__ void unpack_slabs_kernel(const double* __restrict__ src, double* __restrict__ dst, int p, int w,
-                                    int ncols) {
+                                    long long ss, long long rs, int ncols) {
     const long long total = (long long)p * ncols;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(e / ncols);
         const int c = (int)(e - (long long)i * ncols);
         const int b = c / w;
-        dst[e] = src[(long long)b * p * w + (long long)i * w + (c - b * w)];
+        dst[e] = src[(long long)b * ss + (long long)i * rs + (c - b * w)];
     }
 }
 
@@ -928,18 +931,19 @@ __global__ void rowmajor_diag_kernel(const double* __restrict__ src, double* __r
         diag[i] = src[(long long)i * p + i];
 }
 
-__global__ void slab_set_identity_kernel(double* __restrict__ slab, int p, int w, int nblk, int blk0) {
+__global__ void slab_set_identity_kernel(double* __restrict__ slab, int p, int w, long long ss, long long rs, int nblk,
+                                         int blk0) {
     const int c0 = blk0 * w;
     const int c1 = min(p, (blk0 + nblk) * w);
     for (int c = c0 + blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += gridDim.x * blockDim.x) {
         const int b = c / w - blk0;
-        slab[(long long)b * p * w + (long long)c * w + (c - (b + blk0) * w)] = 1.0;
+        slab[(long long)b * ss + (long long)c * rs + (c - (b + blk0) * w)] = 1.0;
     }
 }
 
 // Count exact non-zeros of the strict upper triangle (model.py:249-253).
-__global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, int w, int nblk, int blk0,
-                                       unsigned long long* __restrict__ out) {
+__global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, int w, long long ss, long long rs,
+                                       int nblk, int blk0, unsigned long long* __restrict__ out) {
     unsigned long long local = 0;
     const long long total = (long long)nblk * p * w;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -947,8 +951,9 @@ __global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, i
         const long long b = e / ((long long)p * w);
         const long long rem = e - b * p * w;
         const int i = (int)(rem / w);
-        const long long c = (blk0 + b) * w + (rem - (long long)i * w);
-        if (c < p && i < c && slab[e] != 0.0) ++local;
+        const long long j = rem - (long long)i * w;
+        const long long c = (blk0 + b) * w + j;
+        if (c < p && i < c && slab[b * ss + (long long)i * rs + j] != 0.0) ++local;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(out, local);
@@ -958,10 +963,10 @@ __global__ void slab_edge_count_kernel(const double* __restrict__ slab, int p, i
 // Row i of W is sum_k om[i,k] T[k,:]; each block streams its own slab.
 __global__ void wform_init_csr_kernel(const long long* __restrict__ rowptr, const int* __restrict__ colidx,
                                       const double* __restrict__ vals, const double* __restrict__ Tslab,
-                                      double* __restrict__ Wslab, int p, int w) {
+                                      double* __restrict__ Wslab, int p, int w, long long ss, long long rs) {
     const int b = blockIdx.y;
-    const double* Tb = Tslab + (long long)b * p * w;
-    double* Wb = Wslab + (long long)b * p * w;
+    const double* Tb = Tslab + (long long)b * ss;
+    double* Wb = Wslab + (long long)b * ss;
     const int w2 = w >> 1;
     const long long items = (long long)p * w2;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < items;
@@ -971,11 +976,11 @@ __global__ void wform_init_csr_kernel(const long long* __restrict__ rowptr, cons
         double2 acc = make_double2(0.0, 0.0);
         for (long long e = rowptr[i]; e < rowptr[i + 1]; ++e) {
             const double v = vals[e];
-            const double2 tv = __ldg(reinterpret_cast<const double2*>(Tb + (long long)colidx[e] * w) + j2);
+            const double2 tv = __ldg(reinterpret_cast<const double2*>(Tb + (long long)colidx[e] * rs) + j2);
             acc.x = fma(v, tv.x, acc.x);
             acc.y = fma(v, tv.y, acc.y);
         }
-        reinterpret_cast<double2*>(Wb + (long long)i * w)[j2] = acc;
+        reinterpret_cast<double2*>(Wb + (long long)i * rs)[j2] = acc;
     }
 }
 
@@ -1038,15 +1043,16 @@ static int grid_for(long long total) {
     return (int)g;
 }
 
-cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk, int blk0,
-                              cudaStream_t st) {
-    pack_slabs_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(src, ld, dst, p, w, nblk, blk0);
+cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, long long ss, long long rs,
+                              int nblk, int blk0, cudaStream_t st) {
+    pack_slabs_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(src, ld, dst, p, w, ss, rs, nblk, blk0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, int nblk, int blk0, cudaStream_t st) {
+cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, long long ss, long long rs, int nblk,
+                                int blk0, cudaStream_t st) {
     const int ncols = max(0, min(p, (blk0 + nblk) * w) - blk0 * w);
-    unpack_slabs_kernel<<<grid_for((long long)p * ncols), 256, 0, st>>>(src, dst, p, w, ncols);
+    unpack_slabs_kernel<<<grid_for((long long)p * ncols), 256, 0, st>>>(src, dst, p, w, ss, rs, ncols);
     return cudaGetLastError();
 }
 
@@ -1055,27 +1061,28 @@ cudaError_t launch_rowmajor_diag(const double* src, double* diag, int p, cudaStr
     return cudaGetLastError();
 }
 
-cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, int blk0, cudaStream_t st) {
+cudaError_t launch_slab_identity(double* slab, int p, int w, long long ss, long long rs, int nblk, int blk0,
+                                 cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(slab, 0, sizeof(double) * (size_t)nblk * p * w, st);
     if (e != cudaSuccess) return e;
-    slab_set_identity_kernel<<<grid_for((long long)nblk * w), 256, 0, st>>>(slab, p, w, nblk, blk0);
+    slab_set_identity_kernel<<<grid_for((long long)nblk * w), 256, 0, st>>>(slab, p, w, ss, rs, nblk, blk0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, int blk0, unsigned long long* out,
-                                   cudaStream_t st) {
+cudaError_t launch_slab_edge_count(const double* slab, int p, int w, long long ss, long long rs, int nblk, int blk0,
+                                   unsigned long long* out, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    slab_edge_count_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(slab, p, w, nblk, blk0, out);
+    slab_edge_count_kernel<<<grid_for((long long)nblk * p * w), 256, 0, st>>>(slab, p, w, ss, rs, nblk, blk0, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_wform_init_csr(const long long* rowptr, const int* colidx, const double* vals, const double* Tslab,
-                                  double* Wslab, int p, int w, int nblk, cudaStream_t st) {
+                                  double* Wslab, int p, int w, long long ss, long long rs, int nblk, cudaStream_t st) {
     long long items = (long long)p * (w >> 1);
     int gx = (int)((items + 255) / 256);
     if (gx > 64) gx = 64;
-    wform_init_csr_kernel<<<dim3(gx, nblk), 256, 0, st>>>(rowptr, colidx, vals, Tslab, Wslab, p, w);
+    wform_init_csr_kernel<<<dim3(gx, nblk), 256, 0, st>>>(rowptr, colidx, vals, Tslab, Wslab, p, w, ss, rs);
     return cudaGetLastError();
 }
 

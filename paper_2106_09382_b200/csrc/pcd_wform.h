@@ -112,7 +112,10 @@ struct QbCopies {
 };
 struct QbArgs {
     int p, m, half, w;
-    long long slab;
+    long long slab;        // stride between this launch's slabs (p*w: slab layout; w: row-major layout)
+    int ld;                // row stride of W, T, Om (w: slab layout; the launch's columns: row-major)
+    long long slabT;       // the same two strides for Tfull
+    int ldT;
     double* W;             // this launch's slabs
     const double* T;       // this launch's slabs
     const double* Tfull;   // every slab of T (== T unless a process shard): the cells' T entries
@@ -162,15 +165,17 @@ cudaError_t launch_pcd_wform(const WformArgs& args, int nblk, cudaStream_t st);
 cudaError_t wform_max_blocks(int w, int p, int nblk_tot, int* max_blocks);
 // Slab-layout helpers.  `nblk` slabs of width w starting at global column block
 // blk0 (columns [blk0*w, (blk0+nblk)*w) clipped to p).
-cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, int nblk, int blk0,
-                              cudaStream_t st);
+cudaError_t launch_pack_slabs(const double* src, long long ld, double* dst, int p, int w, long long ss, long long rs,
+                              int nblk, int blk0, cudaStream_t st);
 // Slabs -> row-major p x ncols block (ld = ncols) of the columns the slabs hold.
-cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, int nblk, int blk0, cudaStream_t st);
-cudaError_t launch_slab_identity(double* slab, int p, int w, int nblk, int blk0, cudaStream_t st);
-cudaError_t launch_slab_edge_count(const double* slab, int p, int w, int nblk, int blk0, unsigned long long* out,
-                                   cudaStream_t st);
+cudaError_t launch_unpack_slabs(const double* src, double* dst, int p, int w, long long ss, long long rs, int nblk,
+                                int blk0, cudaStream_t st);
+cudaError_t launch_slab_identity(double* slab, int p, int w, long long ss, long long rs, int nblk, int blk0,
+                                 cudaStream_t st);
+cudaError_t launch_slab_edge_count(const double* slab, int p, int w, long long ss, long long rs, int nblk, int blk0,
+                                   unsigned long long* out, cudaStream_t st);
 cudaError_t launch_wform_init_csr(const long long* rowptr, const int* colidx, const double* vals, const double* Tslab,
-                                  double* Wslab, int p, int w, int nblk, cudaStream_t st);
+                                  double* Wslab, int p, int w, long long ss, long long rs, int nblk, cudaStream_t st);
 // Diagonal of a row-major p x p matrix (the replicated T diagonal).
 cudaError_t launch_rowmajor_diag(const double* src, double* diag, int p, cudaStream_t st);
 
@@ -183,10 +188,13 @@ cudaError_t launch_u2_sweep_exact(double* om, const double* t, int p, double n, 
 cudaError_t launch_cd_sweep_exact(double* om, const double* t, int p, double n, double shrink, cudaStream_t st);
 
 // Diagnostics on the slab-resident estimate, diag.cu.
-cudaError_t launch_optimality(const double* W, const double* Om, int p, int w, double n, double weight,
+cudaError_t launch_optimality(const double* W, const double* Om, int p, int w, long long ss, long long rs, double n,
+                              double weight,
                               double* blk_val, long long* blk_idx, int nblocks, cudaStream_t st);
-cudaError_t launch_triplet_count(const double* Om, int p, int w, int* rowcnt, cudaStream_t st);
-cudaError_t launch_triplet_write(const double* Om, int p, int w, const long long* rowoff, int* ti, int* tj,
+cudaError_t launch_triplet_count(const double* Om, int p, int w, long long ss, long long rs, int* rowcnt,
+                                 cudaStream_t st);
+cudaError_t launch_triplet_write(const double* Om, int p, int w, long long ss, long long rs, const long long* rowoff,
+                                 int* ti, int* tj,
                                  double* tv, cudaStream_t st);
 
 // On-device AR(2) samples (datagen.cu): centred X (n x p row-major); XT (p x n) and mean (p) are scratch.
