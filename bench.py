@@ -52,6 +52,8 @@ sys.path.insert(0, REPO)
 
 LAMS = [0.55, 0.50, 0.45, 0.40, 0.35, 0.30, 0.25, 0.20, 0.15, 0.10]
 METRIC = "sweeps/s (CONCORD-PCD fits, p=5000 n=2000, 10-lambda path)"
+DATA_PATH = ("synthetic: AR(2) truth (datagen.ar2_precision), X ~ N(0, inv(truth)) n=2000 seed 0 (datagen.sample_mvn), "
+             "centred, on the exact-Gram grid of synth.quantize_exact_gram (the reference fixtures' data)")
 UNIT = "sweeps/s"
 
 
@@ -394,7 +396,7 @@ def run_ours(args, d):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": K, "warmup": W,
         "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic: AR(2) truth (datagen.ar2_precision), X ~ N(0, inv(truth)) n=2000 seed 0, centred",
+        "data": DATA_PATH,
         "config": {"workload": workload, "source": "BASELINE.json configs[2] (paper workload)", "p": p, "n": n,
                    "lambdas": lams, "fits_per_step": len(lams), "concurrency": k, "delta_tol": args.delta_tol,
                    "init": "identity",
@@ -588,8 +590,12 @@ def run_reference(args, d):
             "ms_per_step": 1e3 * total_s / K, "higher_is_better": True,
             "scaling": "weak" if args.mode == "path" else "strong", "vs_baseline": None,
             "dtype": "f64", "impl": "reference",
-            "data": f"synthetic: AR(2) truth, X ~ N(0, inv(truth)) n={n} seed 0, centred",
-            "config": {"workload": workload, "p": p, "n": args.n},
+            "data": DATA_PATH if args.mode == "path" else
+                    f"synthetic: AR(2) truth, X ~ N(0, inv(truth)) n={n} seed 0, centred",
+            "config": ({"workload": workload, "source": "BASELINE.json configs[2] (paper workload)", "p": p, "n": args.n,
+                        "lambdas": list(LAMS), "fits_per_step": len(LAMS), "delta_tol": args.delta_tol,
+                        "init": "identity"} if args.mode == "path" else
+                       {"workload": workload, "source": "BASELINE.json configs[3]", "p": p, "n": args.n}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
