@@ -100,6 +100,11 @@ int concord_solver_destroy(concord_solver* s);
 int concord_solver_create_sharded(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
                                   concord_solver** out);
 int concord_solver_layout(concord_solver* s, concord_layout* out);
+/* Chain-warp variant of the blocked kernel for this solver's fits: 6 (default), 4 (apply-heavy:
+ * dense fits), 8 (chain-heavy: sparse fits on a small share of the SMs).  4 and 8 align the roles
+ * to warp groups and redistribute registers between them with setmaxnreg.  Results are bitwise
+ * identical for every variant.  No reference counterpart (a scheduling knob). */
+int concord_solver_set_chain_warps(concord_solver* s, int32_t chain_warps);
 
 /* ---- multi-GPU: one process per GPU, column-sharded --------- */
 /* Shard `rank` of n_shards.  Exchange the handles (all-gather of

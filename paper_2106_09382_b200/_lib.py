@@ -34,7 +34,7 @@ EXPORTS = (
     "concord_solver_check_optimality", "concord_solver_estimate_entries",
     "concord_ar2_data_f64", "concord_solver_gram_from_ar2", "concord_blocked_plan", "concord_device_sm_count",
     "concord_solver_gram_from_raw_data", "concord_center_columns_f64",
-    "concord_tree_data_f64", "concord_solver_gram_from_tree",
+    "concord_tree_data_f64", "concord_solver_gram_from_tree", "concord_solver_set_chain_warps",
 )
 
 ABI_VERSION = 2
@@ -136,6 +136,7 @@ def load(build_if_missing=True):
             "concord_center_columns_f64": ([vp, i64, i64, i32, i32], ctypes.c_int),
             "concord_tree_data_f64": ([i64, i64, ctypes.c_uint64, vp, vp, vp, vp, i32, i32], ctypes.c_int),
             "concord_solver_gram_from_tree": ([vp, i64, ctypes.c_uint64, vp, vp, vp], ctypes.c_int),
+            "concord_solver_set_chain_warps": ([vp, i32], ctypes.c_int),
             "concord_solver_get_gram": ([vp, vp, i32], ctypes.c_int),
             "concord_solver_fit": ([vp, ctypes.POINTER(FitParams), ctypes.POINTER(FitResult), vp, vp, vp],
                                    ctypes.c_int),

@@ -15,8 +15,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libconcord_b200.so")
-SOURCES = ["pcd_wform.cu", "pcd_qblock.cu", "pcd_exact.cu", "gram.cu", "diag.cu", "datagen.cu", "capi.cu"]
-HEADERS = ["common.cuh", "pcd_wform.h"]
+SOURCES = ["pcd_wform.cu", "pcd_qblock.cu", "pcd_qblock_cw4.cu", "pcd_qblock_cw8.cu", "pcd_exact.cu", "gram.cu",
+           "diag.cu", "datagen.cu", "capi.cu"]
+HEADERS = ["common.cuh", "pcd_wform.h", "pcd_qblock_impl.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -131,6 +131,7 @@ struct concord_solver {
     bool qb = false;       // temporally blocked chain (pcd_qblock.cu)
     int qb_D = 0, qb_NB = 0, qb_sr = 0, qb_rd = 0, qb_rl = 0;
     int qb_nbuf = 1, qb_td = 0, qb_ring = 6;  // shared-memory plan of the blocked kernel
+    int qb_cw = QB_CHAIN_WARPS;               // its chain-warp variant (4, 6, 8)
     double* Tfull = nullptr;  // process shard on the blocked kernel: every slab of T (the cells' T entries)
     // storage of W, T, Om: local slab b, row i, slab column j at b * ss + i * ld + j.  Row-major
     // (ss = w, ld = the launch's columns) for the blocked kernel -- every CTA streams the same
@@ -316,26 +317,26 @@ struct QbPlan {
     int D, nbuf, td, ring;
     size_t smem;
 };
-static bool qblock_plan(int p, int nblk, int share, int D, bool allow_overlap, QbPlan* out) {
+static bool qblock_plan(int p, int nblk, int share, int D, bool allow_overlap, int chain_warps, QbPlan* out) {
     const int m = p + (p & 1) - 1;
     if (D < 2) D = 2;
     if (D > QB_DMAX) D = QB_DMAX;
     if (2 * D > m + 1) D = (m + 1) / 2;
-    int cw = qblock_colour_warps(share, D);
+    int cw = qblock_colour_warps(chain_warps, share, D);
     if (const char* e = getenv("CONCORD_QB_CW")) {  // tuning: a negative value fixes the colour group's warps
         const int v = atoi(e);
         cw = v < 0 ? -v : (v > cw ? v : cw);
     }
     int pf_cells = 5;  // part A overlaps the colours when the prefetch group has at most this many cells per thread
     if (const char* e = getenv("CONCORD_QB_PF_CELLS")) pf_cells = atoi(e);
-    const int pf_threads = 32 * (WFORM_CHAIN_WARPS_QB - cw);
+    const int pf_threads = 32 * (chain_warps - cw);
     const bool can_overlap = allow_overlap && pf_threads > 0 && qblock_cellcap(share, D) <= pf_cells * pf_threads;
     static const int plans[][3] = {{2, 1, 6}, {2, 0, 6}, {1, 1, 6}, {1, 0, 6}, {1, 0, 4}, {1, 0, 2}};
     const int td_ok = wform_tdiag_in_smem(p);
     for (const auto& pl : plans) {
         if (pl[0] == 2 && !can_overlap) continue;
         if (pl[1] && !td_ok) continue;
-        const size_t smem = qblock_smem_bytes(p, nblk, share, D, pl[1], pl[0], pl[2]);
+        const size_t smem = qblock_smem_bytes(chain_warps, p, nblk, share, D, pl[1], pl[0], pl[2]);
         if (smem + 2048 <= 227 * 1024) {  // + static shared memory
             *out = QbPlan{D, pl[0], pl[1], pl[2], smem};
             return true;
@@ -354,7 +355,7 @@ int setup_qblock(concord_solver* s) {
     bool allow_overlap = true;
     if (const char* e = getenv("CONCORD_QB_NBUF")) allow_overlap = atoi(e) >= 2;
     QbPlan plan;
-    if (!qblock_plan(p, s->nblk_tot, s->share, D, allow_overlap, &plan)) return CONCORD_OK;  // per-phase kernel
+    if (!qblock_plan(p, s->nblk_tot, s->share, D, allow_overlap, s->qb_cw, &plan)) return CONCORD_OK;  // per-phase kernel
     D = plan.D;
     s->qb_nbuf = plan.nbuf;
     s->qb_td = plan.td;
@@ -362,7 +363,7 @@ int setup_qblock(concord_solver* s) {
     if (const char* e = getenv("CONCORD_QB_RING")) {  // tuning: a deeper ring when it still fits
         const int r = atoi(e);
         if ((r == 2 || r == 4 || r == 6 || r == 8) &&
-            qblock_smem_bytes(p, s->nblk_tot, s->share, plan.D, plan.td, plan.nbuf, r) + 2048 <= 227 * 1024)
+            qblock_smem_bytes(s->qb_cw, p, s->nblk_tot, s->share, plan.D, plan.td, plan.nbuf, r) + 2048 <= 227 * 1024)
             s->qb_ring = r;
     }
     s->qb_D = D;
@@ -564,6 +565,22 @@ int concord_shard_open_peers(concord_solver* s, const void* handles) {
         s->arena_owned[r] = false;
     }
     s->peers_open = true;
+    return CONCORD_OK;
+}
+
+int concord_solver_set_chain_warps(concord_solver* s, int32_t chain_warps) {
+    if (!s) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (!qblock_variant_ok(chain_warps)) return fail(CONCORD_ERR_ARG, "chain_warps must be 4, 6 or 8, got %d", chain_warps);
+    if (!s->qb) return CONCORD_OK;  // the per-phase kernel has one variant
+    const int keep = s->qb_cw;
+    s->qb_cw = chain_warps;
+    const int rc = setup_qblock(s);  // re-plans shared memory for the variant (buffers do not change)
+    if (rc || !s->qb) {
+        s->qb_cw = keep;
+        s->qb = true;
+        setup_qblock(s);
+        return rc ? rc : fail(CONCORD_ERR_ARG, "variant with %d chain warps does not fit shared memory", chain_warps);
+    }
     return CONCORD_OK;
 }
 
@@ -772,6 +789,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.tdiag_smem = s->qb_td;
         q.nbuf = s->qb_nbuf;
         q.colour_warps_min = 1;
+        q.chain_warps = s->qb_cw;
         if (const char* e = getenv("CONCORD_QB_CW")) q.colour_warps_min = atoi(e);
         q.ring_stages = s->qb_ring;
         for (int r = 0; r < s->G; ++r) {
@@ -1219,7 +1237,7 @@ int concord_blocked_plan(int64_t p, int32_t n_sms, concord_blocked_plan_t* out) 
     out->ctas = nblk;
     out->share = share;
     QbPlan plan;
-    if (ip >= 256 && QB_DEFAULT && qblock_plan(ip, nblk, share, QB_DEFAULT_D, true, &plan)) {
+    if (ip >= 256 && QB_DEFAULT && qblock_plan(ip, nblk, share, QB_DEFAULT_D, true, QB_CHAIN_WARPS, &plan)) {
         out->colours_per_barrier = plan.D;
         out->cell_buffers = plan.nbuf;
         out->tdiag_in_smem = plan.td;

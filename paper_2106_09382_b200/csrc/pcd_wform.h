@@ -149,12 +149,31 @@ struct QbArgs {
     int nbuf;              // cell buffers: 2 = next block's cells built during the colours
     int ring_stages;       // cp.async row-ring depth (2, 4 or 6)
     int colour_warps_min;  // lower bound on the colour group's warps (tuning)
+    int chain_warps;       // kernel variant: 4, 6 or 8 chain warps
 };
 int qblock_cellcap(int share, int D);
 int qblock_rmax(int share, int D);
-size_t qblock_smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
-int qblock_colour_warps(int share, int D);
+// Chain-warp variants of the blocked kernel: 6 (default), 4 (apply-heavy), 8 (chain-heavy).
+bool qblock_variant_ok(int chain_warps);
+size_t qblock_smem_bytes(int chain_warps, int p, int nblk, int share, int D, int tdiag_smem, int nbuf,
+                         int ring_stages);
+int qblock_colour_warps(int chain_warps, int share, int D);
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st);
+namespace qb4 {
+size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
+int colour_warps_host(int share, int D);
+cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st);
+}
+namespace qb6 {
+size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
+int colour_warps_host(int share, int D);
+cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st);
+}
+namespace qb8 {
+size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
+int colour_warps_host(int share, int D);
+cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st);
+}
 
 // Lag cap for a slab width (bounded by the stage ring's shared memory) and m.
 int wform_lag_cap(int w, int m);

@@ -200,6 +200,13 @@ class Solver:
         _lib.check(_lib.load().concord_solver_layout(self._h, ctypes.byref(lay)))
         return {f: getattr(lay, f) for f, _ in _lib.Layout._fields_}
 
+    def set_chain_warps(self, chain_warps):
+        """Kernel variant for this solver's fits: 6 chain warps (default), 4 (apply-heavy: dense
+        fits) or 8 (chain-heavy: sparse fits on a small lane).  4 and 8 align the roles to warp
+        groups and move registers between them (setmaxnreg); results are bitwise identical."""
+        _lib.check(_lib.load().concord_solver_set_chain_warps(self._h, int(chain_warps)))
+        self.chain_warps = int(chain_warps)
+
     def set_stream(self, stream_ptr):
         _lib.check(_lib.load().concord_solver_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))
 
@@ -380,9 +387,11 @@ class PathScheduler:
     fits: the slab count never changes the bits.
     """
 
-    def __init__(self, p, device=0, k=2, lanes=None):
+    def __init__(self, p, device=0, k=2, lanes=None, variants=None):
         """k equal lanes of SMs/k slabs, or `lanes`: the SM count of every lane (largest first),
-        e.g. (74, 37, 37) -- the densest fit on the largest lane, the sparse ones on the others."""
+        e.g. (74, 37, 37) -- the densest fit on the largest lane, the sparse ones on the others.
+        `variants`: the kernel's chain warps per lane (Solver.set_chain_warps); default with three
+        or more lanes: 4 on the largest lane, 8 on the others."""
         nsm = _lib.device_sm_count(device)
         if lanes is None:
             # one large lane (9/20 of the device) for the densest fits, the rest split evenly:
@@ -404,6 +413,13 @@ class PathScheduler:
             try:
                 for v in lanes:
                     self.shares.append(Solver(p, device=device, n_blocks=v))
+                # kernel variants per lane (profiles/r02/ab_register_split.log): the largest lane
+                # takes the densest fits -> apply-heavy (4 chain warps); the small lanes run the
+                # latency-bound sparse fits -> chain-heavy (8)
+                if variants is None:
+                    variants = [4] + [8] * (len(lanes) - 1) if len(lanes) >= 3 else [6] * len(lanes)
+                for sv, cw in zip(self.shares, variants):
+                    sv.set_chain_warps(cw)
             except _lib.ConcordError as e:
                 # every lane holds its own T, W and Omega (3 x 8p^2 bytes): when they do not fit
                 # (p=50000: 60 GB each), the path runs one fit at a time on all SMs

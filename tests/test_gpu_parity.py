@@ -449,3 +449,28 @@ def test_virtual_shards_on_the_blocked_kernel(sys_scope, monkeypatch):
                 assert r.iterations == w.iterations and r.edge_count == w.edge_count
                 assert np.array_equal(r.estimate.omega, w.estimate.omega)
                 np.testing.assert_allclose(r.objective_trace, w.objective_trace, rtol=1e-12)
+
+
+@pytest.mark.parametrize("n_blocks", [0, 41])
+def test_kernel_variants_are_bitwise_identical(n_blocks):
+    """The chain-warp variants of the blocked kernel (6 default; 4 apply-heavy and 8 chain-heavy,
+    whose warp groups trade registers with setmaxnreg) evaluate the same FMAs in the same order:
+    bitwise the same estimate, iterations and objective trace, also consecutive fits on one solver."""
+    _, t = synth.problem("ar2", 1000, 500, seed=7)
+    g = cb.GramMatrix(t, 500)
+    outs = {}
+    for cw in (6, 4, 8):
+        with cb.Solver(1000, n_blocks=n_blocks) as s:
+            assert s.layout()["kernel"] == 4
+            s.set_chain_warps(cw)
+            s.set_gram(g)
+            outs[cw] = [s.fit(lam, 1e-5, 500) for lam in (0.3, 0.1)]
+    for cw in (4, 8):
+        for r, w in zip(outs[cw], outs[6]):
+            assert r.iterations == w.iterations and r.edge_count == w.edge_count
+            assert np.array_equal(r.estimate.omega, w.estimate.omega)
+            np.testing.assert_allclose(r.objective_trace, w.objective_trace, rtol=1e-12)
+    from paper_2106_09382_b200 import _lib
+
+    with cb.Solver(1000) as s, pytest.raises(_lib.ConcordError):
+        s.set_chain_warps(5)
