@@ -390,8 +390,7 @@ class PathScheduler:
     def __init__(self, p, device=0, k=2, lanes=None, variants=None):
         """k equal lanes of SMs/k slabs, or `lanes`: the SM count of every lane (largest first),
         e.g. (74, 37, 37) -- the densest fit on the largest lane, the sparse ones on the others.
-        `variants`: the kernel's chain warps per lane (Solver.set_chain_warps); default with three
-        or more lanes: 4 on the largest lane, 8 on the others."""
+        `variants`: the kernel's chain warps per lane (Solver.set_chain_warps; default 6 on all)."""
         nsm = _lib.device_sm_count(device)
         if lanes is None:
             # one large lane (9/20 of the device) for the densest fits, the rest split evenly:
@@ -413,12 +412,11 @@ class PathScheduler:
             try:
                 for v in lanes:
                     self.shares.append(Solver(p, device=device, n_blocks=v))
-                # kernel variants per lane (profiles/r02/ab_register_split.log): the largest lane
-                # takes the densest fits -> apply-heavy (4 chain warps); the small lanes run the
-                # latency-bound sparse fits -> chain-heavy (8)
-                if variants is None:
-                    variants = [4] + [8] * (len(lanes) - 1) if len(lanes) >= 3 else [6] * len(lanes)
-                for sv, cw in zip(self.shares, variants):
+                # kernel variant per lane (Solver.set_chain_warps).  Alone, an apply-heavy dense fit
+                # and chain-heavy sparse fits are 6% / 11% faster, but running concurrently every
+                # combination was slower than the default (profiles/r02/lanes_variants.log), so the
+                # lanes keep 6 chain warps unless told otherwise
+                for sv, cw in zip(self.shares, variants or []):
                     sv.set_chain_warps(cw)
             except _lib.ConcordError as e:
                 # every lane holds its own T, W and Omega (3 x 8p^2 bytes): when they do not fit

@@ -8,7 +8,8 @@ p, n = 5000, 2000
 x = synth.center(synth.sample_mvn(synth.ar2_precision(p), n, seed=0))
 import os
 lanes = [int(v) for v in os.environ.get('LANES', '74,74').split(',')]
-sched = cb.PathScheduler(p, lanes=lanes)
+variants = [int(v) for v in os.environ["VARIANTS"].split(",")] if os.environ.get("VARIANTS") else None
+sched = cb.PathScheduler(p, lanes=lanes, variants=variants)
 sched.full.gram_from_data(cb.DataMatrix(x, centered=True))
 g = sched.full.gram()
 for s in sched.shares:
