@@ -31,6 +31,7 @@ from paper_2106_09382_b200 import synth
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 FIXTURES = sorted(glob.glob(os.path.join(HERE, "golden", "p5000", "ar2_p5000_n2000_l*.npz")))
+EXTRA = os.path.join(HERE, "golden", "p5000")
 
 pytestmark = pytest.mark.gpu
 
@@ -47,7 +48,7 @@ def gram():
 
 
 def _check(rep, fx, label):
-    p = 5000
+    p = int(fx["meta"][0])
     om = rep.estimate.omega
     iu = np.triu_indices(p, 1)
     mask = np.unpackbits(fx["support"], count=iu[0].size).astype(bool)
@@ -94,3 +95,32 @@ def test_p5000_path_lanes_match_reference(gram):
     reps = cb.pcd_path(g, lams, delta_tol=1e-5, max_outer_iterations=5000, concurrency=3)
     for rep, fx in zip(reps, fxs):
         _check(rep, fx, "pcd_path(concurrency=3)")
+
+
+def test_p5001_odd_p_matches_reference():
+    """Odd p at the paper size (p colours per sweep, a phantom partner in every round)."""
+    path = os.path.join(EXTRA, "extra_ar2_p5001_n2000_l0.30.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated (tests/golden/make_golden_p5000_extra.py)")
+    fx = _load(path)
+    x, t = synth.portable_problem("ar2", 5001, 2000, seed=0)
+    assert hashlib.sha256(t.tobytes()).hexdigest() == bytes(fx["tsha"]).decode()
+    rep = cb.pcd_fit(cb.GramMatrix(t, 2000), cb.SolverConfig(lam=0.3, max_outer_iterations=5000))
+    _check(rep, fx, "pcd_fit p=5001")
+
+
+def test_p5000_warm_start_matches_reference(gram):
+    """Warm start at the paper size (SolverConfig.init, model.py:158-166): lambda=0.25 from the
+    lambda=0.30 estimate, as pcd_path(warm_start=True) chains them; the reference started from its
+    own lambda=0.30 estimate, which equals ours to ~1e-15."""
+    path = os.path.join(EXTRA, "extra_ar2_p5000_n2000_l0.25_warm_from_0.30.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated (tests/golden/make_golden_p5000_extra.py)")
+    fx = _load(path)
+    g, tsha = gram
+    assert tsha == bytes(fx["tsha"]).decode()
+    reps = cb.pcd_path(g, [0.30, 0.25], delta_tol=1e-5, max_outer_iterations=5000, warm_start=True)
+    _check(reps[1], fx, "pcd_path(warm_start=True)")
+    first = cb.pcd_fit(g, cb.SolverConfig(lam=0.30, max_outer_iterations=5000))
+    rep = cb.pcd_fit(g, cb.SolverConfig(lam=0.25, max_outer_iterations=5000, init=first.estimate))
+    _check(rep, fx, "pcd_fit(init=lambda 0.30 estimate)")
