@@ -823,6 +823,15 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.want_trace = a.want_trace;
         q.D = s->qb_D;
         q.NB = s->qb_NB;
+        {
+            // Granlund-Montgomery: l = ceil(log2 NB), magic = floor(2^32 (2^l - NB) / NB) + 1,
+            // q = (t + ((b - t) >> 1)) >> (l - 1) with t = umulhi(b, magic), exact for all 32-bit b
+            const unsigned d = (unsigned)s->qb_NB;
+            int l = 0;
+            while ((1ull << l) < d) ++l;
+            q.nb_shift = (d <= 1) ? -1 : l - 1;
+            q.nb_magic = (d <= 1) ? 0u : (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+        }
         q.cellcap = qblock_cellcap(s->share, s->qb_D);
         q.rmax = qblock_rmax(s->share, s->qb_D);
         q.stage_window = 4 * s->qb_D;

@@ -16,8 +16,11 @@ namespace concord {
 // Odd p: id p is the phantom; pairs touching it are skipped (schedule.py:49-55).
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int circle_partner(int x, int k, int m) {
-    if (x == 0) return 1 + (m - 1 - k) % m;
-    int y = 1 + (3 * m - x - 1 - 2 * k) % m;
+    // division-free for 0 <= k < m, 0 <= x <= m: m-1-k is in [0, m) and 3m-x-1-2k in [1, 3m-2]
+    if (x == 0) return m - k;
+    int t = 3 * m - x - 1 - 2 * k;
+    t -= (t >= 2 * m) ? 2 * m : ((t >= m) ? m : 0);
+    const int y = 1 + t;
     return (y == x) ? 0 : y;
 }
 

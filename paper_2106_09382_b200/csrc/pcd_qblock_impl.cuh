@@ -123,9 +123,15 @@ __device__ __forceinline__ double ldcg_if(const double* ptr, bool on) {
 struct Blk {
     int g0, ph0, len, sweep;
 };
-__device__ __forceinline__ Blk block_at(int b, int m, int D, int NB) {
+// b / NB without a division (Granlund-Montgomery; nb_magic / nb_shift precomputed by the host)
+__device__ __forceinline__ int div_nb(int b, unsigned magic, int shift) {
+    if (shift < 0) return b;  // NB == 1
+    const unsigned t = __umulhi((unsigned)b, magic);
+    return (int)((t + (((unsigned)b - t) >> 1)) >> shift);
+}
+__device__ __forceinline__ Blk block_at(int b, int m, int D, int NB, unsigned magic, int shift) {
     Blk k;
-    k.sweep = b / NB;
+    k.sweep = div_nb(b, magic, shift);
     const int j = b - k.sweep * NB;
     k.ph0 = j * D;
     k.len = min(D, m + 1 - k.ph0);
@@ -135,8 +141,8 @@ __device__ __forceinline__ Blk block_at(int b, int m, int D, int NB) {
 // Watermark of the stage of block b: every phase <= C' is already in the staged cells.
 // C'(b) = start of block b-3, minus one: the deltas it needs are known once the chain is at
 // block b-3, so the stager has a block of slack before the chain needs it (at block b-2).
-__device__ __forceinline__ int stage_mark(int b, int m, int D, int NB) {
-    return (b < 3) ? -1 : block_at(b - 3, m, D, NB).g0 - 1;
+__device__ __forceinline__ int stage_mark(int b, int m, int D, int NB, unsigned magic, int shift) {
+    return (b < 3) ? -1 : block_at(b - 3, m, D, NB, magic, shift).g0 - 1;
 }
 
 // Chain warps the colours of a block need: one thread per pair of the widest colour.
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
 
     // ---- stage blocks 0 and 1 from the initial W, Omega (watermark -1)
     for (int bb = 0; bb < 2 && bb < 2 * NB; ++bb) {
-        const Blk k = block_at(bb, m, D, NB);
+        const Blk k = block_at(bb, m, D, NB, a.nb_magic, a.nb_shift);
         for (int idx = tid; idx < k.len * wl; idx += kThreads) {
             const int i = idx / wl, j = idx - i * wl;
             const int Q = k.g0 + i;
@@ -588,11 +594,11 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         // order.  Blocks alternate between two cell buffers and two layouts.  Threads
         // [0, gs) take part, synchronised by the named barrier `bar_id`.
         auto cells_a = [&](int B, int gs, int bar_id) {
-            const Blk kB = block_at(B, m, D, NB);
+            const Blk kB = block_at(B, m, D, NB, a.nb_magic, a.nb_shift);
             const bool hdB = (kB.ph0 + kB.len - 1 == m);
             const int nbcB = kB.len - (hdB ? 1 : 0);
-            const int CpB = stage_mark(B, m, D, NB);
-            const int hiA = (B >= 1) ? block_at(B - 1, m, D, NB).g0 : 0;
+            const int CpB = stage_mark(B, m, D, NB, a.nb_magic, a.nb_shift);
+            const int hiA = (B >= 1) ? block_at(B - 1, m, D, NB, a.nb_magic, a.nb_shift).g0 : 0;
             const int na = hiA - (CpB + 1);
             Layout& L = s_ly[B & 1];
             const int cb = (a.nbuf == 2) ? (B & 1) * a.cellcap : 0;
@@ -706,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
         int blk = 0;
         while (true) {
             const long long t0 = PCLK();
-            const Blk k = block_at(blk, m, D, NB);
+            const Blk k = block_at(blk, m, D, NB, a.nb_magic, a.nb_shift);
             if (tc == 0) {
                 wait_counter(barL, a.bar_base + (unsigned long long)(blk + 1) * (unsigned long long)nblk, blk, a.hang,
                              a.sys_scope);
@@ -748,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             }
             // ---- cells, part B (on the critical path): deltas of the previous block
             {
-                const int hiA = (blk >= 1) ? block_at(blk - 1, m, D, NB).g0 : 0;
+                const int hiA = (blk >= 1) ? block_at(blk - 1, m, D, NB, a.nb_magic, a.nb_shift).g0 : 0;
                 const int nbv = k.g0 - hiA;
                 const int ntotB = L.ncell + (has_diag ? 2 * (q_hi - q_lo) : 0);
                 // two cells per step: both cells' ring loads, then both cells' T loads, back to back
@@ -1054,12 +1060,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             // stage up to cblk+3.  Its watermark C' must be <= E-1 (deltas known) and the
             // window (C, C'] must still be in the delta ring.
             const int sb = staged + 1;
-            const int Cp = stage_mark(sb, m, D, NB);
+            const int Cp = stage_mark(sb, m, D, NB, a.nb_magic, a.nb_shift);
             const bool can_stage = stopg < 0 && cblk >= 0 && sb <= cblk + 3 && Cp <= E - 1 && C >= Cp - a.stage_window;
             // and the block after it in the same pass when it is eligible too and the batches are
             // small (the apply then gets a block ahead of the chain's needs and its latency-bound
             // batches grow to two blocks; dense batches are bandwidth-bound and gain nothing)
-            const int Cp2 = stage_mark(sb + 1, m, D, NB);
+            const int Cp2 = stage_mark(sb + 1, m, D, NB, a.nb_magic, a.nb_shift);
             const bool can2 = can_stage && last_total <= 256 && sb + 1 <= cblk + 3 && Cp2 <= E - 1 &&
                               C >= Cp2 - a.stage_window;
             if (!have && !can_stage) {
@@ -1098,14 +1104,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             // ---- stage block sb: cells brought forward from this slab's watermark C to C'
             if (can_stage) {
                 const long long ts = PCLK();
-                const Blk kb0 = block_at(sb, m, D, NB);
-                const Blk kb1 = block_at(sb + 1, m, D, NB);
+                const Blk kb0 = block_at(sb, m, D, NB, a.nb_magic, a.nb_shift);
+                const Blk kb1 = block_at(sb + 1, m, D, NB, a.nb_magic, a.nb_shift);
                 const int n0 = kb0.len * wl;
                 const int nst = n0 + (can2 ? kb1.len * wl : 0);
                 for (int idx2 = ta; idx2 < nst; idx2 += kApply) {
                     const bool second = idx2 >= n0;
                     const Blk kb = second ? kb1 : kb0;
-                    const int Cp = second ? Cp2 : stage_mark(sb, m, D, NB);
+                    const int Cpx = second ? Cp2 : Cp;
                     const int idx = second ? idx2 - n0 : idx2;
                     const int i = idx / wl, j = idx - i * wl;
                     const int Q = kb.g0 + i;
@@ -1114,15 +1120,15 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if (x < 0) continue;
                     double val = __ldcg(Wb + (long long)x * ld + j);
                     const double om = __ldcg(Ob + (long long)x * ld + j);
-                    // deltas of phases C+1 .. Cp, eight at a time: ring loads back to back, then the
+                    // deltas of phases C+1 .. Cpx, eight at a time: ring loads back to back, then the
                     // T entries of the phases that moved row x (predicated, back to back), then the FMAs
                     int rslot = (C + 1) % a.rd;
                     PartnerWalk pw(x, (C + 1) % (m + 1), m);
-                    for (int j0 = C + 1; j0 <= Cp; j0 += 8) {
+                    for (int j0 = C + 1; j0 <= Cpx; j0 += 8) {
                         double dj[8], tj[8];
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            dj[u] = ldcg_if(dringL + (size_t)rslot * p + x, j0 + u <= Cp);
+                            dj[u] = ldcg_if(dringL + (size_t)rslot * p + x, j0 + u <= Cpx);
                             rslot = (rslot + 1 == a.rd) ? 0 : rslot + 1;
                         }
                         unsigned mk = 0u;

@@ -137,6 +137,8 @@ struct QbArgs {
     double n, shrink, delta_tol;
     int max_iter, want_trace;
     int D, NB;             // phases per block, blocks per sweep
+    unsigned nb_magic;     // b / NB as a multiply-shift (host: qblock_div_magic)
+    int nb_shift;          // -1 when NB == 1
     int cellcap, rmax;     // shared-memory sizing of the block cells
     int stage_window;      // max phases a stage may be brought forward over
     double* rec_delta;
