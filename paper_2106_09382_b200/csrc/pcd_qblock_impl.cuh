@@ -91,7 +91,13 @@ struct PartnerWalk {
     int x, m, v, ph;
     __device__ __forceinline__ PartnerWalk(int x_, int ph_, int m_) : x(x_), m(m_), ph(ph_) {
         const int k = (ph_ == m_) ? 0 : ph_;
-        v = (x_ == 0) ? (m_ - 1 - k) % m_ : (3 * m_ - x_ - 1 - 2 * k) % m_;
+        // division-free: m-1-k is in [0, m), 3m-x-1-2k in [1, 3m-2] (0 <= k < m, 1 <= x <= m)
+        if (x_ == 0) {
+            v = m_ - 1 - k;
+        } else {
+            v = 3 * m_ - x_ - 1 - 2 * k;
+            v -= (v >= 2 * m_) ? 2 * m_ : ((v >= m_) ? m_ : 0);
+        }
     }
     __device__ __forceinline__ int y() const {
         if (ph == m) return x;
@@ -656,8 +662,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     }
                     c = x;
                 }
-                const int cs = c / w;  // slab of column c
-                const double* Tc = a.Tfull + (long long)cs * a.slabT + (c - cs * w);
+                // column c of T: row-major storage (slabT == w) is plain column indexing
+                const double* Tc = (a.slabT == w) ? a.Tfull + c
+                                                  : a.Tfull + (long long)(c / w) * a.slabT + (c - (c / w) * w);
                 const size_t so = (size_t)L.slot[d] * p + c;
                 double val = __ldcg(stWL + so);
                 const double om = __ldcg(stOL + so);
@@ -668,7 +675,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 for (int i = 0; i < kDMax - 1; ++i)
                     tin[i] = ldcg_if(stTL + ((size_t)L.slot[d] * (kDMax - 1) + i) * p + c, i < d);
                 {
-                    int pos = (x == 0) ? 0 : 1 + (x - 1 + kB.ph0) % m;
+                    int pos = x - 1 + kB.ph0;  // in [0, 2m): one conditional subtraction for the mod
+                    pos = (x == 0) ? 0 : 1 + (pos >= m ? pos - m : pos);
                     for (int i = 0; i < d; ++i) {
                         const int qi = (pos == 0 || pos == m) ? 0 : min(pos, m - pos);
                         sm.cQ()[(size_t)(cb + ci) * dm1 + i] = (short)(qi - L.lo[i]);
@@ -784,8 +792,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         for (int h = 0; h < 2; ++h) {
                             const int ci = c0i + h * kChain;
                             const int c = mask[h] ? sm.cC()[cb + ci] : 0;
-                            const int cs = c / w;  // slab of column c
-                            const double* Tc = a.Tfull + (long long)cs * a.slabT + (c - cs * w);
+                            const double* Tc = (a.slabT == w)
+                                                   ? a.Tfull + c
+                                                   : a.Tfull + (long long)(c / w) * a.slabT + (c - (c / w) * w);
                             PartnerWalk pw(max(xs[h], 0), L.phb, m);
 #pragma unroll
                             for (int u = 0; u < kDMax; ++u) {
