@@ -309,10 +309,18 @@ __device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d
     }
     bar_apply();
     const int items = 2 * nent * w2;
+    // item idx = (half-entry he, chunk j2), stepped without division
+    const int sq = kApply / w2, sr = kApply - sq * w2;
+    int che = ta / w2, cj2 = ta - (ta / w2) * w2;
     for (int idx = ta; idx < items; idx += kApply) {
-        const int he = idx / w2;
+        const int he = che, j2 = cj2;
+        che += sq;
+        cj2 += sr;
+        if (cj2 >= w2) {
+            cj2 -= w2;
+            ++che;
+        }
         if (!s_first[he]) continue;
-        const int j2 = idx - he * w2;
         const int2 rs0 = L_rs[he >> 1];
         const int dst = (he & 1) ? rs0.y : rs0.x;
         double2* wp = reinterpret_cast<double2*>(Wb) + (long long)dst * ld2 + j2;
@@ -1117,12 +1125,28 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const Blk kb1 = block_at(sb + 1, m, D, NB, a.nb_magic, a.nb_shift);
                 const int n0 = kb0.len * wl;
                 const int nst = n0 + (can2 ? kb1.len * wl : 0);
+                // cell (phase i of the block, slab column j) stepped without division; the ring slots
+                // of the delta walk and the block's stage slots hoisted out of the loop
+                const int rslot0 = (C + 1) % a.rd, phw0 = (C + 1) % (m + 1);
+                const int wld = max(wl, 1);  // a padding slab (no columns) runs no iterations
+                const int sq = kApply / wld, sr = kApply - sq * wld;
+                int ci = ta / wld, cj = ta - (ta / wld) * wld;
+                bool second = false;
                 for (int idx2 = ta; idx2 < nst; idx2 += kApply) {
-                    const bool second = idx2 >= n0;
+                    if (!second && idx2 >= n0) {
+                        second = true;
+                        ci = (idx2 - n0) / wld;
+                        cj = (idx2 - n0) - ci * wld;
+                    }
+                    const int i = ci, j = cj;
+                    ci += sq;
+                    cj += sr;
+                    if (cj >= wld) {
+                        cj -= wld;
+                        ++ci;
+                    }
                     const Blk kb = second ? kb1 : kb0;
                     const int Cpx = second ? Cp2 : Cp;
-                    const int idx = second ? idx2 - n0 : idx2;
-                    const int i = idx / wl, j = idx - i * wl;
                     const int Q = kb.g0 + i;
                     const int c = c0 + j;
                     const int x = pub_row(kb.ph0 + i, c, m, p);
@@ -1131,8 +1155,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const double om = __ldcg(Ob + (long long)x * ld + j);
                     // deltas of phases C+1 .. Cpx, eight at a time: ring loads back to back, then the
                     // T entries of the phases that moved row x (predicated, back to back), then the FMAs
-                    int rslot = (C + 1) % a.rd;
-                    PartnerWalk pw(x, (C + 1) % (m + 1), m);
+                    int rslot = rslot0;
+                    PartnerWalk pw(x, phw0, m);
                     for (int j0 = C + 1; j0 <= Cpx; j0 += 8) {
                         double dj[8], tj[8];
 #pragma unroll
@@ -1224,14 +1248,23 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     }
                     bar_apply();
                     const int items = (iend - i0) * w2;
+                    // item (row ii of the chunk, column pair j2) of each unrolled slot, stepped
+                    // without division
+                    int cii[kUnroll], cjj[kUnroll];
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        cii[u] = (u * kApply + ta) / w2;
+                        cjj[u] = (u * kApply + ta) - cii[u] * w2;
+                    }
+                    const int dsq = (kApply * kUnroll) / w2, dsr = kApply * kUnroll - dsq * w2;
                     for (int base = 0; base < items; base += kApply * kUnroll) {
                         double2 wv[kUnroll], tv[kUnroll], ov[kUnroll];
 #pragma unroll
                         for (int u = 0; u < kUnroll; ++u) {
                             const int idx = base + u * kApply + ta;
                             if (idx < items) {
-                                const int ii = idx / w2;
-                                const int j2 = idx - ii * w2;
+                                const int ii = cii[u];
+                                const int j2 = cjj[u];
                                 const long long off = (long long)(i0 + ii) * ld + 2 * j2;
                                 wv[u] = __ldcg(reinterpret_cast<const double2*>(Wb + off));
                                 if (sm.L_d()[ii] != 0.0) tv[u] = __ldcg(reinterpret_cast<const double2*>(Tb + off));
@@ -1242,8 +1275,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         for (int u = 0; u < kUnroll; ++u) {
                             const int idx = base + u * kApply + ta;
                             if (idx < items) {
-                                const int ii = idx / w2;
-                                const int j2 = idx - ii * w2;
+                                const int ii = cii[u];
+                                const int j2 = cjj[u];
                                 const int i = i0 + ii;
                                 const long long off = (long long)i * ld + 2 * j2;
                                 const double d = sm.L_d()[ii];
@@ -1268,6 +1301,15 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 } else if (dg0 | dg1) {
                                     Ob[off + (dg0 ? 0 : 1)] = sm.L_new()[ii];
                                 }
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            cii[u] += dsq;
+                            cjj[u] += dsr;
+                            if (cjj[u] >= w2) {
+                                cjj[u] -= w2;
+                                ++cii[u];
                             }
                         }
                     }
