@@ -896,14 +896,25 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 // ---- publish the own pairs of all colours: delta ring, non-zero delta lists
                 {
                     const int nown = q_hi - q_lo;
+                    const int nwn = max(nown, 1);
+                    // item (colour d, own pair q) stepped without division
+                    const int pdq = ng / nwn, pdr = ng - pdq * nwn;
+                    int pd = gt / nwn, pr = gt - (gt / nwn) * nwn;
                     for (int base = 0; base < nbc * nown; base += ng) {
                         const int idx = base + gt;
                         const bool live = idx < nbc * nown;
                         int d = 0, q = 0, r = 0, s = 0;
                         double dl = 0.0, nv = 0.0;
+                        const int d_it = pd, r_it = pr;
+                        pd += pdq;
+                        pr += pdr;
+                        if (pr >= nwn) {
+                            pr -= nwn;
+                            ++pd;
+                        }
                         if (live) {
-                            d = idx / nown;
-                            q = q_lo + (idx - d * nown);
+                            d = d_it;
+                            q = q_lo + r_it;
                             round_pair(q, m, m - 1 - (k.ph0 + d), r, s);
                             dl = sm.sd()[(size_t)d * a.rmax + (q - L.lo[d])];
                             nv = sm.snv()[d * a.share + (q - q_lo)];
@@ -1101,9 +1112,20 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
             // ---- segment heads (count + first entry) of the batch's colours: copied
             // asynchronously into shared memory while this thread stages (below); every
             // thread then reads back only the heads it copied
+            // segment (batch phase jb, CTA) stepped without division; ring slot of phase k0 + jb
+            const int k0rl = k0 % a.rl;
+            const int hsq = kApply / nsh, hsr = kApply - hsq * nsh;
+            int hjb = ta / nsh, hcta = ta - (ta / nsh) * nsh;
             for (int idx = ta; idx < nseg; idx += kApply) {
-                const int jb = idx / nsh;
-                const int seg = ((k0 + jb) % a.rl) * nblk + (idx - jb * nsh);
+                const int jb = hjb;
+                const int slot = (k0rl + jb >= a.rl) ? k0rl + jb - a.rl : k0rl + jb;
+                const int seg = slot * nblk + hcta;
+                hjb += hsq;
+                hcta += hsr;
+                if (hcta >= nsh) {
+                    hcta -= nsh;
+                    ++hjb;
+                }
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
                                  (unsigned)__cvta_generic_to_shared(sm.s_off() + idx)),
                              "l"(lcntL + seg)
@@ -1206,8 +1228,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 t_stage += PCLK() - ts;
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");
+            hjb = ta / nsh;
+            hcta = ta - hjb * nsh;
             for (int idx = ta; idx < nseg; idx += kApply) {
-                const int jb = idx / nsh;
+                const int jb = hjb;
+                hjb += hsq;
+                hcta += hsr;
+                if (hcta >= nsh) {
+                    hcta -= nsh;
+                    ++hjb;
+                }
                 const int cnt = sm.s_off()[idx];
                 if (cnt > 1) s_multi = 1;
                 if (cnt == 1) {
