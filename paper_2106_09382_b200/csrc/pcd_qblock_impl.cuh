@@ -1150,6 +1150,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 // cell (phase i of the block, slab column j) stepped without division; the ring slots
                 // of the delta walk and the block's stage slots hoisted out of the loop
                 const int rslot0 = (C + 1) % a.rd, phw0 = (C + 1) % (m + 1);
+                const int sl0 = kb0.g0 % a.sr, sl1 = kb1.g0 % a.sr;  // stage slots of the blocks' first phases
                 const int wld = max(wl, 1);  // a padding slab (no columns) runs no iterations
                 const int sq = kApply / wld, sr = kApply - sq * wld;
                 int ci = ta / wld, cj = ta - (ta / wld) * wld;
@@ -1169,7 +1170,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     }
                     const Blk kb = second ? kb1 : kb0;
                     const int Cpx = second ? Cp2 : Cp;
-                    const int Q = kb.g0 + i;
+                    int qs = (second ? sl1 : sl0) + i;  // stage slot of phase kb.g0 + i (i < D < sr)
+                    qs -= (qs >= a.sr) ? a.sr : 0;
                     const int c = c0 + j;
                     const int x = pub_row(kb.ph0 + i, c, m, p);
                     if (x < 0) continue;
@@ -1204,7 +1206,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             for (int u = 0; u < 8; ++u) pw.next();
                         }
                     }
-                    const size_t so = (size_t)(Q % a.sr) * p + c;
+                    const size_t so = (size_t)qs * p + c;
                     QB_COPIES(cp) {
                         a.x.stW[cp][so] = val;
                         a.x.stO[cp][so] = om;
@@ -1222,7 +1224,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         }
 #pragma unroll
                         for (int ii = 0; ii < kDMax - 1; ++ii)
-                            if (ii < i) QB_COPIES(cp) a.x.stT[cp][((size_t)(Q % a.sr) * (kDMax - 1) + ii) * p + c] = tv[ii];
+                            if (ii < i) QB_COPIES(cp) a.x.stT[cp][((size_t)qs * (kDMax - 1) + ii) * p + c] = tv[ii];
                     }
                 }
                 t_stage += PCLK() - ts;
