@@ -629,13 +629,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 }
                 L.cb[kDMax] = nc;
                 L.ncell = nc;
-                for (int d = 0; d <= kDMax; ++d) L.slot[d] = (kB.g0 + d) % a.sr;
+                // ring slots of the block's phases: one modulo per ring, then wraps (d <= D < ring sizes)
+                const int gs0 = kB.g0 % a.sr, gd0 = kB.g0 % a.rd, gl0 = kB.g0 % a.rl;
+                for (int d = 0; d <= kDMax; ++d) L.slot[d] = (gs0 + d >= a.sr) ? gs0 + d - a.sr : gs0 + d;
                 for (int d = 0; d < kDMax; ++d) {
-                    L.rdc[d] = (kB.g0 + d) % a.rd;
-                    L.lsl[d] = (kB.g0 + d) % a.rl;
+                    L.rdc[d] = (gd0 + d >= a.rd) ? gd0 + d - a.rd : gd0 + d;
+                    L.lsl[d] = (gl0 + d >= a.rl) ? gl0 + d - a.rl : gl0 + d;
                 }
+            } else if (tc == 1) {  // the delta-walk starts, in parallel with thread 0
                 L.rd0 = (CpB + 1) % a.rd;
                 L.ph0w = (CpB + 1) % (m + 1);
+            } else if (tc == 2) {
                 L.rdb = hiA % a.rd;
                 L.phb = hiA % (m + 1);
             }
