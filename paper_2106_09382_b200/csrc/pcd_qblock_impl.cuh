@@ -283,7 +283,7 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
 // loads W[dst, chunk] once, the T chunks of the whole chain at once, and applies the FMAs in
 // phase order -- the same operations, in the same order, as phase-by-phase passes, in one
 // round trip instead of one per phase.
-__device__ __forceinline__ void apply_chains(const int2* L_rs, const double* L_d, const int* L_ph, int nent, int w2,
+__device__ __noinline__ void apply_chains(const int2* L_rs, const double* L_d, const int* L_ph, int nent, int w2,
                                              int ld2, double* __restrict__ Wb, const double* __restrict__ Tb, short* s_next,
                                              unsigned char* s_first, int ta) {
     for (int he = ta; he < 2 * nent; he += kApply) {
@@ -1453,12 +1453,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         const int conflict = s_conflict;
                         if (!conflict) {
                             ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, 0, e1 - e0, w2, Wb, Tb, sm.ring(), ta);
+                        } else if (e1 - e0 <= kChainN) {
+                            // few entries: per-row chains, one round trip instead of one pass per phase
+                            apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), e1 - e0, w2, ld2, Wb, Tb, s_next, s_first, ta);
                         } else {
                             for (int jb = 0; jb < nb; ++jb) {
                                 const int lo = max(sm.s_off()[jb * nsh], e0) - e0;
                                 const int hi = min(sm.s_off()[(jb + 1) * nsh], e1) - e0;
-                                if (lo < hi) ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, lo, hi, w2, Wb, Tb, sm.ring(), ta);
-                                bar_apply();
+                                if (lo < hi) {  // uniform across the apply warps: no pass, no barrier
+                                    ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, lo, hi, w2, Wb, Tb, sm.ring(), ta);
+                                    bar_apply();
+                                }
                             }
                         }
                         bar_apply();
