@@ -824,13 +824,17 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.D = s->qb_D;
         q.NB = s->qb_NB;
         {
-            // Granlund-Montgomery: l = ceil(log2 NB), magic = floor(2^32 (2^l - NB) / NB) + 1,
+            // Granlund-Montgomery: l = ceil(log2 d), magic = floor(2^32 (2^l - d) / d) + 1,
             // q = (t + ((b - t) >> 1)) >> (l - 1) with t = umulhi(b, magic), exact for all 32-bit b
-            const unsigned d = (unsigned)s->qb_NB;
-            int l = 0;
-            while ((1ull << l) < d) ++l;
-            q.nb_shift = (d <= 1) ? -1 : l - 1;
-            q.nb_magic = (d <= 1) ? 0u : (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+            auto magic = [](unsigned d, unsigned& mg, int& sh) {
+                int l = 0;
+                while ((1ull << l) < d) ++l;
+                sh = (d <= 1) ? -1 : l - 1;
+                mg = (d <= 1) ? 0u : (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+            };
+            magic((unsigned)s->qb_NB, q.nb_magic, q.nb_shift);
+            magic((unsigned)s->w, q.w_magic, q.w_shift);
+            magic((unsigned)(s->w / 2), q.w2_magic, q.w2_shift);
         }
         q.cellcap = qblock_cellcap(s->share, s->qb_D);
         q.rmax = qblock_rmax(s->share, s->qb_D);

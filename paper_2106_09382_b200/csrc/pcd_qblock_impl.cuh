@@ -198,13 +198,15 @@ __device__ int apply_scan(int* s, int n, int ta, int* s_wsum) {
 // registers allow. Each thread only reads the
 // slots it filled, so no barrier is needed; cp.async.wait_group orders them.
 __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double* L_d, const int* L_ph, int only,
-                                                 int e_lo, int e_hi, int w2, long long ld2, double* __restrict__ Wb,
+                                                 int e_lo, int e_hi, int w2, unsigned per_magic, int per_shift,
+                                                 long long ld2, double* __restrict__ Wb,
                                                  const double* __restrict__ Tb, double2* ring, int ta, int S) {
     const int per = 2 * w2;
     const int items = (e_hi - e_lo) * per;
     const int nmine = items > ta ? (items - ta + kApply - 1) / kApply : 0;
     // item idx = ta + i * kApply -> (entry q, position rem in the entry), stepped without division
-    const int dq = kApply / per, dr = kApply - dq * per;
+    // x / per as a multiply-shift (per = w; host-computed magic): no division per pass
+    const int dq = div_nb(kApply, per_magic, per_shift), dr = kApply - dq * per;
     struct Cursor {
         int q, rem;
     };
@@ -224,7 +226,8 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
         off_w = (h ? rs.y : rs.x) * ld2 + j2;
         off_t = (h ? rs.x : rs.y) * ld2 + j2;
     };
-    Cursor ci{ta / per, ta - (ta / per) * per};  // next item to issue
+    const int tq = div_nb(ta, per_magic, per_shift);
+    Cursor ci{tq, ta - tq * per};  // next item to issue
     Cursor cc = ci;                               // next item to complete
     int si = 0, sc = 0;  // ring slots of the next issue / the next completion
     auto issue = [&]() {
@@ -284,6 +287,7 @@ __device__ __forceinline__ void apply_rows_async(const int2* L_rs, const double*
 // phase order -- the same operations, in the same order, as phase-by-phase passes, in one
 // round trip instead of one per phase.
 __device__ __noinline__ void apply_chains(const int2* L_rs, const double* L_d, const int* L_ph, int nent, int w2,
+                                          unsigned w2_magic, int w2_shift,
                                              int ld2, double* __restrict__ Wb, const double* __restrict__ Tb, short* s_next,
                                              unsigned char* s_first, int ta) {
     for (int he = ta; he < 2 * nent; he += kApply) {
@@ -310,8 +314,8 @@ __device__ __noinline__ void apply_chains(const int2* L_rs, const double* L_d, c
     bar_apply();
     const int items = 2 * nent * w2;
     // item idx = (half-entry he, chunk j2), stepped without division
-    const int sq = kApply / w2, sr = kApply - sq * w2;
-    int che = ta / w2, cj2 = ta - (ta / w2) * w2;
+    const int sq = div_nb(kApply, w2_magic, w2_shift), sr = kApply - sq * w2;
+    int che = div_nb(ta, w2_magic, w2_shift), cj2 = ta - che * w2;
     for (int idx = ta; idx < items; idx += kApply) {
         const int he = che, j2 = cj2;
         che += sq;
@@ -357,7 +361,7 @@ __device__ __noinline__ void apply_chains(const int2* L_rs, const double* L_d, c
 }
 
 #define ROWS(Lrs, Ld, Lph, only, lo, hi, w2_, Wb_, Tb_, ring_, ta_) \
-    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, ld2, Wb_, Tb_, ring_, ta_, a.ring_stages)
+    apply_rows_async(Lrs, Ld, Lph, only, lo, hi, w2_, a.w_magic, a.w_shift, ld2, Wb_, Tb_, ring_, ta_, a.ring_stages)
 
 #define QB_COPIES_RT(r) _Pragma("unroll") for (int r = 0; r < WFORM_MAX_SHARDS; ++r) if (r < a.G)
 // In the kernel: one copy unless the launch is sharded (kShard), so the unsharded instance carries
@@ -1400,7 +1404,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if (!s_conflict) {
                         ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, 0, nent, w2, Wb, Tb, sm.ring(), ta);
                     } else if (nent <= kChainN) {
-                        apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), nent, w2, ld2, Wb, Tb, s_next, s_first, ta);
+                        apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), nent, w2, a.w2_magic, a.w2_shift, ld2, Wb, Tb, s_next, s_first,
+                                     ta);
                     } else {
                         for (int jb = 0; jb < nb; ++jb) {  // rows repeat across phases: phase by phase
                             ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), jb, 0, nent, w2, Wb, Tb, sm.ring(), ta);
@@ -1455,7 +1460,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                             ROWS(sm.L_rs(), sm.L_d(), sm.L_ph(), -1, 0, e1 - e0, w2, Wb, Tb, sm.ring(), ta);
                         } else if (e1 - e0 <= kChainN) {
                             // few entries: per-row chains, one round trip instead of one pass per phase
-                            apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), e1 - e0, w2, ld2, Wb, Tb, s_next, s_first, ta);
+                            apply_chains(sm.L_rs(), sm.L_d(), sm.L_ph(), e1 - e0, w2, a.w2_magic, a.w2_shift, ld2, Wb, Tb,
+                                         s_next, s_first, ta);
                         } else {
                             for (int jb = 0; jb < nb; ++jb) {
                                 const int lo = max(sm.s_off()[jb * nsh], e0) - e0;

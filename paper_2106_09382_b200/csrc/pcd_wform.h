@@ -137,8 +137,10 @@ struct QbArgs {
     double n, shrink, delta_tol;
     int max_iter, want_trace;
     int D, NB;             // phases per block, blocks per sweep
-    unsigned nb_magic;     // b / NB as a multiply-shift (host: qblock_div_magic)
+    unsigned nb_magic;     // b / NB as a multiply-shift (host-computed, Granlund-Montgomery)
     int nb_shift;          // -1 when NB == 1
+    unsigned w_magic, w2_magic;  // the same for the slab width w and w/2 (row-stream cursors)
+    int w_shift, w2_shift;
     int cellcap, rmax;     // shared-memory sizing of the block cells
     int stage_window;      // max phases a stage may be brought forward over
     double* rec_delta;
