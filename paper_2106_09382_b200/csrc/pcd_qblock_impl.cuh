@@ -60,6 +60,12 @@ constexpr int kBatch = WFORM_BATCH;
 constexpr int kUnroll = 2;
 constexpr int kDMax = QB_DMAX;
 constexpr int kChainN = 32;   // batches with row conflicts up to this many entries: per-row chains
+#ifndef QB_POLL_NS
+#define QB_POLL_NS 20         // back-off of the chain's spin loops (barrier, own stager)
+#endif
+#ifndef QB_IDLE_NS
+#define QB_IDLE_NS 32         // back-off of the idle apply warps
+#endif
 
 __device__ __forceinline__ void bar_chain() { asm volatile("bar.sync 1, %0;" ::"n"(kChain) : "memory"); }
 __device__ __forceinline__ void bar_apply() { asm volatile("bar.sync 2, %0;" ::"n"(kApply) : "memory"); }
@@ -391,7 +397,7 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* ctr, unsi
     int spins = 0;
     do {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-        if (v < target) __nanosleep(20);  // leave the issue slots to the apply warps of this SMSP
+        if (QB_POLL_NS && v < target) __nanosleep(QB_POLL_NS);  // leave issue slots to this SMSP's apply warps
         if (++spins == 4096) {
             spins = 0;
             if (globaltimer_ns() - t0 > kHangNs) hang_report(hang, 0, blk, (long long)v, (long long)target, 0, 0);
@@ -1020,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     const long long tw0 = PCLK();
                     const unsigned long long g0t = globaltimer_ns();
                     while (ld_acquire_cta(&s_staged) < blk + 2) {
-                        __nanosleep(20);
+                        if (QB_POLL_NS) __nanosleep(QB_POLL_NS);
                         if (globaltimer_ns() - g0t > kHangNs) hang_report(a.hang, 1, blk, blk + 2, ld_vol(&s_staged), 0, 0);
                     }
                     t_c3 += PCLK() - tw0;
@@ -1112,7 +1118,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                     if (idle_since == 0) idle_since = globaltimer_ns();
                     else if (globaltimer_ns() - idle_since > kHangNs) hang_report(a.hang, 2, cblk, C, E, staged, stopg);
                 }
-                __nanosleep(32);
+                if (QB_IDLE_NS) __nanosleep(QB_IDLE_NS);
                 continue;
             }
             idle_since = 0;
