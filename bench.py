@@ -7,9 +7,9 @@ Workload (BASELINE.json configs[2], the paper workload): AR(2) truth,
 p=5000, n=2000 synthetic samples (datagen.py restated in synth.py, seed 0),
 the 10-value lambda path 0.55, 0.50, ..., 0.10.  One STEP = the whole path:
 ten complete cold-start CONCORD-PCD fits (identity init, delta_tol 1e-5),
-scheduled by the package's PathScheduler -- --concurrency k (default 3)
-lanes, each a solver on its own share of the SMs (k=3: 66/41/41 on a B200; own
-stream and host thread), pull the fits densest first (one latency-bound fit leaves
+scheduled by the package's PathScheduler -- --concurrency k (default 4)
+lanes, each a solver on its own share of the SMs (k=4: 66/28/27/27 on a B200;
+own stream and host thread), pull the fits densest first (one latency-bound fit leaves
 most of a B200 idle; longest job first balances the lanes).  --concurrency 1 runs every
 fit on all SMs, one after the other.
 The metric is sweeps/s (outer iterations per second, BASELINE "sweeps/sec"),
@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--delta-tol", type=float, default=1e-5)
-    ap.add_argument("--concurrency", type=int, default=3,
+    ap.add_argument("--concurrency", type=int, default=4,
                     help="fits run at a time per GPU, each on SMs/k (path mode); 1 = one fit on all SMs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

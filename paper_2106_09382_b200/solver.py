@@ -350,7 +350,7 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
     (a non-converged fit is returned with converged=False, not raised).
 
     concurrency=k (cold mode) runs the fits on k lanes, each a solver on its
-    own share of the SMs (k=3 on a B200: 66/41/41), densest lambda first
+    own share of the SMs (k=3 on a B200: 66/41/41; k=4: 66/28/27/27, the bench's), densest lambda first
     (`PathScheduler`); the results are bitwise those of sequential fits.
     """
     if concurrency > 1:
@@ -395,7 +395,9 @@ class PathScheduler:
         if lanes is None:
             # one large lane (9/20 of the device) for the densest fits, the rest split evenly:
             # the sparse fits are latency-bound, so smaller lanes lose little per fit and add
-            # lanes (p=5000 path on 148 SMs: 74/74 -> 3.15 s, 74/37/37 -> 2.67 s, 66/41/41 ->
+            # lanes (round 2, final kernel: 66/28/27/27 -> 2.34 s, 66/41/41 -> 2.40-2.43 s,
+            # 66/21/21/20/20 -> 2.67 s, 70/26/26/26 -> 2.69 s; profiles/r02/lanes_k45.log.  Round 1:
+            # p=5000 path on 148 SMs: 74/74 -> 3.15 s, 74/37/37 -> 2.67 s, 66/41/41 ->
             # 2.55 s, 60/30/30/28 -> 2.62 s; profiles/r01/v6/lane_split_sweep.log)
             if k <= 1:
                 lanes = []
@@ -403,7 +405,8 @@ class PathScheduler:
                 lanes = [nsm // 2, nsm // 2]
             else:
                 big = nsm * 9 // 20
-                lanes = [big] + [(nsm - big) // (k - 1)] * (k - 1)
+                rest = nsm - big  # split as evenly as possible over the other lanes
+                lanes = [big] + [rest // (k - 1) + (1 if j < rest % (k - 1) else 0) for j in range(k - 1)]
         lanes = sorted((int(v) for v in lanes), reverse=True)
         if sum(lanes) > nsm or any(v < 1 for v in lanes):
             raise ValueError(f"lanes {lanes} do not fit the device's {nsm} SMs")
