@@ -9,7 +9,7 @@ on the portable exact Gram (synth.portable_problem: the same T bits on every
 machine, pinned here by its sha256).
 
 For every fixture lambda, through both the single-fit drop-in
-(`pcd_fit`) and the lambda-path lanes (`pcd_path(concurrency=3)`):
+(`pcd_fit`) and the lambda-path lanes (`pcd_path(concurrency=4)`, the bench's):
 * identical iteration count and edge count,
 * identical support (every exact zero of the reference is an exact zero here),
 * max |Omega - Omega_ref| <= 1e-9 * max |Omega_ref| (tolerance stated by
@@ -88,13 +88,13 @@ def test_p5000_fit_matches_reference(gram, path):
 
 
 def test_p5000_path_lanes_match_reference(gram):
-    """The bench's scheduler: every fixture lambda in one pcd_path(concurrency=3) call."""
+    """The bench's scheduler: every fixture lambda in one pcd_path(concurrency=4) call."""
     g, tsha = gram
     fxs = [_load(f) for f in FIXTURES]
     lams = [float(fx["meta"][2]) for fx in fxs]
-    reps = cb.pcd_path(g, lams, delta_tol=1e-5, max_outer_iterations=5000, concurrency=3)
+    reps = cb.pcd_path(g, lams, delta_tol=1e-5, max_outer_iterations=5000, concurrency=4)
     for rep, fx in zip(reps, fxs):
-        _check(rep, fx, "pcd_path(concurrency=3)")
+        _check(rep, fx, "pcd_path(concurrency=4)")
 
 
 def test_p5001_odd_p_matches_reference():
