@@ -835,6 +835,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
             magic((unsigned)s->qb_NB, q.nb_magic, q.nb_shift);
             magic((unsigned)s->w, q.w_magic, q.w_shift);
             magic((unsigned)(s->w / 2), q.w2_magic, q.w2_shift);
+            magic((unsigned)s->nblk_tot, q.nblk_magic, q.nblk_shift);
         }
         q.cellcap = qblock_cellcap(s->share, s->qb_D);
         q.rmax = qblock_rmax(s->share, s->qb_D);

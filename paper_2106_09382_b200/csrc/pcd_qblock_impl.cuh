@@ -1439,10 +1439,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                                 if (sm.s_off()[mid] <= e) lo = mid;
                                 else hi = mid;
                             }
-                            const int jb = lo / nsh;
+                            const int jb = div_nb(lo, a.nblk_magic, a.nblk_shift);  // lo / nsh
                             const int rank = e - sm.s_off()[lo];
-                            const size_t at =
-                                ((size_t)((k0 + jb) % a.rl) * nblk + (lo - jb * nsh)) * a.share + rank;
+                            const int slot = (k0rl + jb >= a.rl) ? k0rl + jb - a.rl : k0rl + jb;
+                            const size_t at = ((size_t)slot * nblk + (lo - jb * nsh)) * a.share + rank;
                             const int2 rs = __ldcg(lrsL + at);
                             const double2 dn = __ldcg(ldnL + at);
                             // segments with one entry had their Omega cells written above

@@ -141,6 +141,8 @@ struct QbArgs {
     int nb_shift;          // -1 when NB == 1
     unsigned w_magic, w2_magic;  // the same for the slab width w and w/2 (row-stream cursors)
     int w_shift, w2_shift;
+    unsigned nblk_magic;   // and for the CTA count (segments per phase of the delta lists)
+    int nblk_shift;
     int cellcap, rmax;     // shared-memory sizing of the block cells
     int stage_window;      // max phases a stage may be brought forward over
     double* rec_delta;
