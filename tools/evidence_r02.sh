@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 evidence in one gpurun call (final kernel): smoke, bench, reference arm, ncu launch list,
 # lambda-path DRAM traffic, one --set full capture of the dense fit on the full device.
-o=gpurun_out/ev_r02; mkdir -p $o
+o=${EV_OUT:-gpurun_out/ev_r02}; mkdir -p $o
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $o/gpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.log 2>&1; echo "smoke rc=$?" >> $o/status.txt
 timeout 900 python bench.py --steps 10 --warmup 3 > $o/bench.json 2> $o/bench.err; echo "bench rc=$?" >> $o/status.txt
