@@ -54,3 +54,28 @@ def test_lane_errors_reach_the_caller():
 
     with pytest.raises(RuntimeError, match="boom"):
         sched.run([0.5, 0.2, 0.3, 0.1], fit_one)
+
+
+def test_default_lane_splits(monkeypatch):
+    """k lanes on a 148-SM B200: 9/20 of the SMs for the densest fits, the rest split as evenly as
+    possible (k=4 is the bench's 66/28/27/27; profiles/r02/lanes_k45.log)."""
+    from paper_2106_09382_b200 import solver
+
+    made = []
+
+    class FakeSolver:
+        def __init__(self, p, device=0, n_blocks=0):
+            made.append(n_blocks)
+
+        def set_chain_warps(self, cw):
+            pass
+
+    monkeypatch.setattr(solver._lib, "device_sm_count", lambda device: 148)
+    monkeypatch.setattr(solver, "Solver", FakeSolver)
+    assert PathScheduler(5000, k=2).lanes == [74, 74]
+    assert PathScheduler(5000, k=3).lanes == [66, 41, 41]
+    assert PathScheduler(5000, k=4).lanes == [66, 28, 27, 27]
+    assert PathScheduler(5000, k=5).lanes == [66, 21, 21, 20, 20]
+    assert sum(PathScheduler(5000, k=4).lanes) == 148
+    with pytest.raises(ValueError):
+        PathScheduler(5000, lanes=[100, 60])
