@@ -71,6 +71,8 @@ def parse():
                     help="fits run at a time per GPU, each on SMs/k (path mode); 1 = one fit on all SMs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-handover", action="store_true",
+                    help="lanes keep their SMs to the end (no hand-over of idle lanes to running fits)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
     ap.add_argument("--cpu-validate", action="store_true",
                     help="also run one complete reference fit at lambda=0.3 on the host (minutes)")
@@ -317,19 +319,30 @@ def run_ours(args, d):
     sched.set_gram(g)  # every lane's solver (the full-device one is created on demand)
     lams = list(LAMS)
 
-    def one_fit(sv, lam):
-        rc, res, deltas, objs, secs = sv.fit_raw(lam, args.delta_tol, 5000, trace=True)
+    def one_seg(sv, lam, done):
+        # one launch of the fit kernel: the whole fit, or the part of it run on one lane size when
+        # the scheduler hands a lane's SMs over to it (PathScheduler.run_segmented)
+        rc, res, deltas, objs, secs = sv.fit_raw(lam, args.delta_tol, 5000 - done, trace=True)
         nnz = np.zeros(res.iterations, dtype=np.int64)
         cnt = ctypes_int()
         _lib.check(_lib.load().concord_solver_sweep_stats(sv._h, _lib.ptr(nnz), res.iterations, cnt))
-        return (lam, int(res.iterations), float(res.kernel_ms), nnz, bool(res.converged), int(res.edge_count),
-                int(res.n_blocks), int(res.slab_width))
+        return rc, int(res.iterations), (int(res.n_blocks), int(res.iterations), float(res.kernel_ms), nnz,
+                                         bool(res.converged), int(res.edge_count), int(res.slab_width))
+
+    def finish(sv, lam, segs):
+        last = segs[-1]
+        return (lam, sum(g[1] for g in segs), sum(g[2] for g in segs), np.concatenate([g[3] for g in segs]),
+                last[4], last[5], segs[0][0], segs[0][6], segs)
+
+    def one_fit(sv, lam):
+        rc, _, seg = one_seg(sv, lam, 0)
+        return finish(sv, lam, [seg])
 
     def frac(sv, f):
         return float(f[3].sum()) / (f[1] * (p * (p - 1) / 2))
 
     def step(out):
-        out.extend(sched.run(lams, one_fit))
+        out.extend(sched.run_segmented(lams, one_seg, finish, handover=not args.no_handover))
 
     for i in range(W):
         step([])
@@ -359,10 +372,11 @@ def run_ours(args, d):
     # stream).  With k lanes the launches overlap on disjoint SM sets, so the device-level HBM
     # utilisation (all fits' bytes / the steps' device time) is reported beside it, as is every
     # lambda's own launch (on its lane's SMs) and two fits alone on the full device.
-    kern_ms = [f[2] for f in fits]
-    bytes_per = [algorithmic_bytes(p, f[3]) for f in fits]
+    kern_ms = [g[2] for f in fits for g in f[8]]  # per launch (a handed-over fit has several)
     avg_ms = sum(kern_ms) / len(kern_ms)
-    avg_bytes = sum(bytes_per) / len(bytes_per)
+    avg_bytes = sum(algorithmic_bytes(p, g[3]) for f in fits for g in f[8]) / len(kern_ms)
+    bytes_per = [algorithmic_bytes(p, f[3]) for f in fits]
+    n_launch = len(kern_ms)
     peak, peak_src = measured_peak_hbm()
     achieved = avg_bytes / (avg_ms / 1e3) / 1e9
     device_gbs = sum(bytes_per) / (elapsed_ms / 1e3) / 1e9
@@ -372,7 +386,8 @@ def run_ours(args, d):
         ms = sum(f[2] for f, _ in sel) / len(sel)
         gbs = sel[0][1] / (ms / 1e3) / 1e9
         per_lambda[f"{lam:.2f}"] = {"ctas": sel[0][0][6], "ms": round(ms, 3), "algorithmic_gb": round(sel[0][1] / 1e9, 2),
-                                    "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+                                    "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                                    "launches": [[[g[0], g[1]] for g in f[8]] for f, _ in sel][-1]}
     full = {}
     sf = sched.full
     sf.set_stream(streams[0].cuda_stream)
@@ -416,8 +431,10 @@ def run_ours(args, d):
                      "per_lambda": per_lambda, "full_device_fits": full,
                      "note": "bytes = sum over sweeps of 48p*nnz_k per colour + 24p per colour + 32p^2 diag/objective"
                              "; achieved = bytes per launch / average launch duration (each launch on its lane's "
-                             "SMs only)"},
-        "gpu_launches": 3 * len(fits),
+                             "SMs only; per_lambda.launches = [CTAs, sweeps] of each launch of the fit's last run)"},
+        "handovers_per_step": (n_launch - len(fits)) / K,
+        # per fit: identity, fit kernel, edge count; per hand-over: 2 x (unpack + pack) + fit + edge count
+        "gpu_launches": 3 * len(fits) + 6 * (n_launch - len(fits)),
         "clocks": clk,
     }
 

@@ -32,6 +32,7 @@ extern "C" {
 
 /* Return codes. */
 #define CONCORD_OK 0
+#define CONCORD_YIELDED 1              /* the fit stopped at a sweep end on request; resumable   */
 #define CONCORD_ERR_ARG (-1)           /* bad dimension / argument (DimensionError, ValueError) */
 #define CONCORD_NOT_CONVERGED (-2)     /* iteration cap hit; outputs are valid (NotConverged)   */
 #define CONCORD_ERR_CUDA (-3)          /* CUDA runtime error                                    */
@@ -133,6 +134,29 @@ int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where);
 int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord_fit_result* res,
                        double* delta_trace, double* objective_trace, double* sweep_seconds);
 int concord_solver_get_omega(concord_solver* s, double* omega_out, int32_t where);
+/* ---- moving a running fit to a solver with more SMs (no reference counterpart: the
+ * lambda-path scheduler's lane hand-over, python/paper_2106_09382_b200/solver.py) ---
+ * request_yield(on=1): the blocked fit running on this solver (or its next one) stops at the
+ * end of its current sweep unless that sweep converged or hit max_iter; concord_solver_fit then
+ * returns CONCORD_YIELDED with the sweeps run so far.  Thread-safe (a mapped host flag); the
+ * flag stays set until request_yield(s, 0).  Unsharded solvers only.
+ * export_state: Omega and the maintained W = Omega T as p x p row-major.
+ * import_state: the next fit on this solver continues from (Omega, W) instead of the identity /
+ * omega_init; the continuation is bitwise the uninterrupted fit (W is carried, not recomputed),
+ * for any pair of slab layouts. */
+int concord_solver_request_yield(concord_solver* s, int32_t on);
+int concord_solver_export_state(concord_solver* s, double* omega_out, double* w_out, int32_t where);
+int concord_solver_import_state(concord_solver* s, const double* omega, const double* w, int32_t where);
+/* The two steps above device to device: dst (same p, device and Gram, any slab count) continues
+ * src's yielded fit with its next concord_solver_fit.  Enqueued on dst's stream after src's
+ * stream drained; src is unchanged.  dst == src: the next fit resumes in place. */
+int concord_solver_take_state(concord_solver* dst, concord_solver* src);
+/* Allocate now what fits of up to max_iter sweeps and state moves allocate lazily (the p x p
+ * scratch, the per-sweep records): a solver that joins a running path must not allocate (or
+ * free) device memory on the way, which can wait for the other lanes' kernels. */
+int concord_solver_reserve(concord_solver* s, int32_t max_iter);
+/* dst's T (and n) := src's, device to device (any two slab layouts, same p and device). */
+int concord_solver_copy_gram(concord_solver* dst, concord_solver* src);
 /* Per-sweep objective partial sums of this solver's columns for the last fit:
  * parts[3*i .. 3*i+2] = (<W,Omega>, sum_{i<j}|omega_ij|, sum log omega_ii)
  * (a shard's partials add up across shards). */

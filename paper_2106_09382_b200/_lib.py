@@ -12,6 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CONCORD_LIB_PATH") or os.path.join(PKG, "libconcord_b200.so")
 
 CONCORD_OK = 0
+CONCORD_YIELDED = 1
 CONCORD_ERR_ARG = -1
 CONCORD_NOT_CONVERGED = -2
 CONCORD_ERR_CUDA = -3
@@ -35,6 +36,9 @@ EXPORTS = (
     "concord_ar2_data_f64", "concord_solver_gram_from_ar2", "concord_blocked_plan", "concord_device_sm_count",
     "concord_solver_gram_from_raw_data", "concord_center_columns_f64",
     "concord_tree_data_f64", "concord_solver_gram_from_tree", "concord_solver_set_chain_warps",
+    "concord_solver_request_yield", "concord_solver_export_state", "concord_solver_import_state",
+    "concord_solver_take_state", "concord_solver_copy_gram",
+    "concord_solver_reserve",
 )
 
 ABI_VERSION = 2
@@ -137,6 +141,12 @@ def load(build_if_missing=True):
             "concord_tree_data_f64": ([i64, i64, ctypes.c_uint64, vp, vp, vp, vp, i32, i32], ctypes.c_int),
             "concord_solver_gram_from_tree": ([vp, i64, ctypes.c_uint64, vp, vp, vp], ctypes.c_int),
             "concord_solver_set_chain_warps": ([vp, i32], ctypes.c_int),
+            "concord_solver_request_yield": ([vp, i32], ctypes.c_int),
+            "concord_solver_export_state": ([vp, vp, vp, i32], ctypes.c_int),
+            "concord_solver_import_state": ([vp, vp, vp, i32], ctypes.c_int),
+            "concord_solver_take_state": ([vp, vp], ctypes.c_int),
+            "concord_solver_copy_gram": ([vp, vp], ctypes.c_int),
+            "concord_solver_reserve": ([vp, i32], ctypes.c_int),
             "concord_solver_get_gram": ([vp, vp, i32], ctypes.c_int),
             "concord_solver_fit": ([vp, ctypes.POINTER(FitParams), ctypes.POINTER(FitResult), vp, vp, vp],
                                    ctypes.c_int),

@@ -90,8 +90,8 @@ ArenaLayout arena_layout(int p, int rd, int rl, int nblk_tot, int share, int qb_
     o = align256(o + sizeof(int) * (size_t)rl * nblk_tot);
     L.bar = o;
     o = align256(o + sizeof(unsigned long long));
-    L.dmax = o;
-    o = align256(o + sizeof(unsigned long long) * WFORM_DMAX_RING);
+    L.dmax = o;  // [WFORM_DMAX_RING] max |delta| per sweep, then [WFORM_DMAX_RING] yield words (blocked kernel)
+    o = align256(o + sizeof(unsigned long long) * 2 * WFORM_DMAX_RING);
     if (qb_sr > 0) {
         L.qb_stW = o;
         o = align256(o + sizeof(double) * (size_t)qb_sr * p);
@@ -139,6 +139,8 @@ struct concord_solver {
     // ld = w) for the per-phase kernel.  ssT / ldT: the same for Tfull.
     long long ss = 0, ld = 0, ssT = 0, ldT = 0;
     long long* hang = nullptr;  // mapped host memory: the fit kernels' watchdog report
+    volatile int* yield = nullptr;  // mapped host flag: the running blocked fit stops at its next sweep end
+    bool resume = false;            // the next fit continues from an imported (Omega, W) state
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     double* T = nullptr;
@@ -367,6 +369,8 @@ int setup_qblock(concord_solver* s) {
             s->qb_ring = r;
     }
     s->qb_D = D;
+    CK(qblock_reserve_smem(s->qb_cw, qblock_smem_bytes(s->qb_cw, p, s->nblk_tot, s->share, D, s->qb_td, s->qb_nbuf,
+                                                        s->qb_ring)));
     s->qb_NB = (m + 1 + D - 1) / D;
     s->qb_sr = 4 * D + 4;
     s->qb_rd = 8 * D + 8;
@@ -456,6 +460,8 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
     CKC(cudaMemsetAsync(s->Om, 0, sizeof(double) * tot, s->stream));
     CKC(cudaHostAlloc((void**)&s->hang, 8 * sizeof(long long), cudaHostAllocMapped));
     memset(s->hang, 0, 8 * sizeof(long long));
+    CKC(cudaHostAlloc((void**)&s->yield, sizeof(int), cudaHostAllocMapped));
+    s->yield[0] = 0;
     CKC(dalloc(&s->tdiag, ip));
     CKC(dalloc(&s->diagd, (size_t)s->nblk_launch * ip));
     {
@@ -584,6 +590,103 @@ int concord_solver_set_chain_warps(concord_solver* s, int32_t chain_warps) {
     return CONCORD_OK;
 }
 
+int concord_solver_request_yield(concord_solver* s, int32_t on) {
+    if (!s || !s->yield) return fail(CONCORD_ERR_ARG, "solver is NULL");
+    s->yield[0] = on ? 1 : 0;
+    return CONCORD_OK;
+}
+
+int concord_solver_export_state(concord_solver* s, double* omega_out, double* w_out, int32_t where) {
+    if (!s || !omega_out || !w_out) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (s->G > 1 || s->rank >= 0) return fail(CONCORD_ERR_ARG, "state export needs an unsharded solver");
+    DeviceGuard g(s->dev);
+    int rc = download_slabs(s, s->Om, omega_out, where);
+    if (rc) return rc;
+    return download_slabs(s, s->W, w_out, where);
+}
+
+int concord_solver_import_state(concord_solver* s, const double* omega, const double* w, int32_t where) {
+    if (!s || !omega || !w) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (s->G > 1 || s->rank >= 0) return fail(CONCORD_ERR_ARG, "state import needs an unsharded solver");
+    if (!s->have_gram) return fail(CONCORD_ERR_ARG, "no Gram matrix set");
+    DeviceGuard g(s->dev);
+    const size_t bytes = sizeof(double) * (size_t)s->p * s->p;
+    const double* src[2] = {omega, w};
+    double* dst[2] = {s->Om, s->W};
+    for (int k = 0; k < 2; ++k) {
+        const double* d = src[k];
+        if (where == CONCORD_HOST) {
+            int rc = ensure_stage(s);
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(s->stage, src[k], bytes, cudaMemcpyHostToDevice, s->stream));
+            d = s->stage;
+        }
+        CK(cudaMemsetAsync(dst[k], 0, sizeof(double) * (size_t)s->nblk_launch * s->slab, s->stream));
+        CK(launch_pack_slabs(d, s->p, dst[k], s->p, s->w, s->ss, s->ld, s->nblk_launch, s->blk0, s->stream));
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    s->resume = true;
+    return CONCORD_OK;
+}
+
+int concord_solver_reserve(concord_solver* s, int32_t max_iter) {
+    if (!s) return fail(CONCORD_ERR_ARG, "solver is NULL");
+    if (max_iter < 1) return fail(CONCORD_ERR_ARG, "max_iter must be at least 1");
+    DeviceGuard g(s->dev);
+    int rc = ensure_stage(s);
+    if (rc) return rc;
+    return ensure_records(s, max_iter);
+}
+
+int concord_solver_copy_gram(concord_solver* dst, concord_solver* src) {
+    if (!dst || !src) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (dst == src) return fail(CONCORD_ERR_ARG, "source and destination are the same solver");
+    if (dst->p != src->p || dst->dev != src->dev) return fail(CONCORD_ERR_ARG, "solvers differ in p or device");
+    if (dst->G > 1 || dst->rank >= 0 || src->G > 1 || src->rank >= 0)
+        return fail(CONCORD_ERR_ARG, "Gram copy needs unsharded solvers");
+    if (!src->have_gram) return fail(CONCORD_ERR_ARG, "source has no Gram matrix");
+    DeviceGuard g(dst->dev);
+    CK(cudaStreamSynchronize(src->stream));
+    int rc = ensure_stage(dst);
+    if (rc) return rc;
+    CK(launch_unpack_slabs(src->T, dst->stage, src->p, src->w, src->ss, src->ld, src->nblk_launch, src->blk0,
+                           dst->stream));
+    rc = set_gram_rowmajor(dst, dst->stage, CONCORD_DEVICE);
+    if (rc) return rc;
+    dst->n = src->n;
+    return CONCORD_OK;
+}
+
+int concord_solver_take_state(concord_solver* dst, concord_solver* src) {
+    if (!dst || !src) return fail(CONCORD_ERR_ARG, "NULL argument");
+    if (dst == src) {  // continue in place: the next fit resumes from this solver's own state
+        dst->resume = true;
+        return CONCORD_OK;
+    }
+    if (dst->p != src->p || dst->dev != src->dev)
+        return fail(CONCORD_ERR_ARG, "solvers differ in p or device (%d/%d vs %d/%d)", dst->p, dst->dev, src->p,
+                    src->dev);
+    if (dst->G > 1 || dst->rank >= 0 || src->G > 1 || src->rank >= 0)
+        return fail(CONCORD_ERR_ARG, "state hand-over needs unsharded solvers");
+    if (!dst->have_gram || !src->have_gram || dst->n != src->n) return fail(CONCORD_ERR_ARG, "Gram matrices differ");
+    DeviceGuard g(dst->dev);
+    CK(cudaStreamSynchronize(src->stream));
+    int rc = ensure_stage(dst);
+    if (rc) return rc;
+    const double* from[2] = {src->Om, src->W};
+    double* to[2] = {dst->Om, dst->W};
+    const size_t tot = (size_t)dst->nblk_launch * dst->slab;
+    for (int k = 0; k < 2; ++k) {  // src slabs -> row-major p x p scratch -> dst slabs, on dst's stream
+        CK(cudaMemsetAsync(to[k], 0, sizeof(double) * tot, dst->stream));  // padding as after a cold start
+        CK(launch_unpack_slabs(from[k], dst->stage, src->p, src->w, src->ss, src->ld, src->nblk_launch, src->blk0,
+                               dst->stream));
+        CK(launch_pack_slabs(dst->stage, dst->p, to[k], dst->p, dst->w, dst->ss, dst->ld, dst->nblk_launch, dst->blk0,
+                             dst->stream));
+    }
+    dst->resume = true;
+    return CONCORD_OK;
+}
+
 int concord_solver_layout(concord_solver* s, concord_layout* out) {
     if (!s || !out) return fail(CONCORD_ERR_ARG, "NULL argument");
     out->p = s->p;
@@ -617,6 +720,7 @@ int concord_solver_destroy(concord_solver* s) {
     }
     cudaFree(s->edges);
     if (s->hang) cudaFreeHost(s->hang);
+    if (s->yield) cudaFreeHost((void*)s->yield);
     cudaFree(s->status);
     cudaFree(s->rec_delta);
     cudaFree(s->rec_obj);
@@ -710,7 +814,11 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     const size_t tot = (size_t)s->nblk_launch * s->slab;
 
     CK(cudaEventRecord(s->ev[0], s->stream));
-    if (prm->omega_init) {
+    if (s->resume) {
+        // continue a yielded fit: Omega and W as concord_solver_import_state left them
+        s->resume = false;  // consumed (also when rejected below)
+        if (prm->omega_init) return fail(CONCORD_ERR_ARG, "omega_init given while an imported state is pending");
+    } else if (prm->omega_init) {
         rc = init_warm(s, prm->omega_init, prm->init_where);
         if (rc) return rc;
     } else {
@@ -847,6 +955,8 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         q.status = a.status;
         q.prof = a.prof;
         q.hang = a.hang;
+        q.yield = nullptr;
+        if (s->G == 1) CK(cudaHostGetDevicePointer((void**)&q.yield, (void*)s->yield, 0));
         CK(launch_pcd_qblock(q, s->nblk_launch, s->stream));
     } else {
         CK(launch_pcd_wform(a, s->nblk_launch, s->stream));
@@ -950,7 +1060,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
     CK(cudaEventElapsedTime(&kernel_ms, s->ev[1], s->ev[2]));
     if (res) {
         res->iterations = iters;
-        res->converged = status[1];
+        res->converged = status[1] == 1 ? 1 : 0;
         res->final_delta = iters > 0 ? dl[iters - 1] : INFINITY;
         res->edge_count = (int64_t)edges;
         res->kernel_ms = kernel_ms;
@@ -958,6 +1068,7 @@ int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord
         res->n_blocks = s->nblk_tot;
         res->slab_width = s->w;
     }
+    if (status[1] == 2) return CONCORD_YIELDED;
     if (!status[1]) {
         fail(CONCORD_NOT_CONVERGED, "no convergence after %d outer iterations, final delta %.3e", iters,
              iters > 0 ? dl[iters - 1] : INFINITY);

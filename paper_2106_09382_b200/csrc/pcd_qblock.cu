@@ -29,6 +29,12 @@ int qblock_colour_warps(int chain_warps, int share, int D) {
     return qb6::colour_warps_host(share, D);
 }
 
+cudaError_t qblock_reserve_smem(int chain_warps, size_t smem) {
+    if (chain_warps == 4) return qb4::reserve_smem(smem);
+    if (chain_warps == 8) return qb8::reserve_smem(smem);
+    return qb6::reserve_smem(smem);
+}
+
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st) {
     if (args.chain_warps == 4) return qb4::launch(args, nblk, st);
     if (args.chain_warps == 8) return qb8::launch(args, nblk, st);

@@ -757,17 +757,23 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                 const int it = k.sweep - 1;
                 const double dmax_all =
                     __longlong_as_double((long long)__ldcg(dmaxL + (a.it_base + it) % WFORM_DMAX_RING));
-                const bool stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter);
+                // a yield request (CTA 0 sampled the host flag before closing the sweep) stops a fit
+                // that would go on; the state is then exactly the one after sweep it (resumable)
+                const bool yld = __ldcg(dmaxL + WFORM_DMAX_RING + (a.it_base + it) % WFORM_DMAX_RING) != 0ull;
+                const bool stop = (dmax_all < a.delta_tol) || (it + 1 >= a.max_iter) || yld;
                 if (bl == 0 && tc == 0) {
                     a.rec_delta[it] = dmax_all;
                     a.rec_time[it + 1] = globaltimer_ns();
                 }
-                if (b == 0 && tc == 0)  // recycle the accumulator of sweep it+2 (last read at sweep it-2)
-                    QB_COPIES(r) a.x.dmax[r][(a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
+                if (b == 0 && tc == 0)  // recycle the accumulators of sweep it+2 (last read at sweep it-2)
+                    QB_COPIES(r) {
+                        a.x.dmax[r][(a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
+                        a.x.dmax[r][WFORM_DMAX_RING + (a.it_base + it + 2) % WFORM_DMAX_RING] = 0ull;
+                    }
                 if (stop) {
                     if (tc == 0) {
                         s_iters = it + 1;
-                        s_conv = dmax_all < a.delta_tol;
+                        s_conv = (dmax_all < a.delta_tol) ? 1 : ((it + 1 < a.max_iter && yld) ? 2 : 0);
                         __threadfence_block();
                         st_vol(&s_stop, k.g0 - 1);
                     }
@@ -1016,6 +1022,8 @@ __global__ void __launch_bounds__(kThreads, 1) pcd_qblock_kernel(QbArgs a) {
                         QB_COPIES(cp)
                             atomicMax(a.x.dmax[cp] + (a.it_base + k.sweep) % WFORM_DMAX_RING,
                                       (unsigned long long)__double_as_longlong(mb));
+                        if (b == 0 && a.yield != nullptr && *a.yield != 0)
+                            QB_COPIES(cp) a.x.dmax[cp][WFORM_DMAX_RING + (a.it_base + k.sweep) % WFORM_DMAX_RING] = 1ull;
                         atomicAdd(reinterpret_cast<unsigned long long*>(a.rec_nnz + k.sweep), (unsigned long long)nbk);
                     }
                 }
@@ -1541,26 +1549,44 @@ size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, i
 // Warps of the colour group for a CTA share (the chain warps the colours need).
 int colour_warps_host(int share, int D) { return colour_warps(share, D); }
 
+const void* kernel_fn(bool prof, bool shard) {
+    return prof ? (shard ? (const void*)pcd_qblock_kernel<true, true> : (const void*)pcd_qblock_kernel<true, false>)
+                : (shard ? (const void*)pcd_qblock_kernel<false, true> : (const void*)pcd_qblock_kernel<false, false>);
+}
+
+// Raise the kernel's shared-memory limit only when needed: setting a function attribute while
+// another fit runs the kernel on another stream waits for that fit, so solvers reserve their
+// launch's bytes when they are created (reserve_smem), not at their first launch.
+cudaError_t raise_smem(size_t smem, bool prof, bool shard) {
+    static std::mutex mu;
+    static size_t set_bytes[4] = {0, 0, 0, 0};
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = set_bytes[(prof ? 2 : 0) + (shard ? 1 : 0)];
+    if (smem > cur) {
+        cudaError_t e = cudaFuncSetAttribute(kernel_fn(prof, shard), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        cur = smem;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t reserve_smem(size_t smem) {
+    for (int v = 0; v < 4; ++v) {
+        cudaError_t e = raise_smem(smem, v >= 2, v & 1);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st) {
     const size_t smem =
         smem_bytes(args.p, args.nblk_tot, args.share, args.D, args.tdiag_smem, args.nbuf, args.ring_stages);
     const bool shard = args.G > 1;
-    const void* fn = args.prof ? (shard ? (const void*)pcd_qblock_kernel<true, true>
-                                        : (const void*)pcd_qblock_kernel<true, false>)
-                               : (shard ? (const void*)pcd_qblock_kernel<false, true>
-                                        : (const void*)pcd_qblock_kernel<false, false>);
+    const void* fn = kernel_fn(args.prof != nullptr, shard);
     {
-        // raise the kernel's shared-memory limit only when needed: setting a function attribute
-        // while another fit runs the kernel on another stream serialises the two
-        static std::mutex mu;
-        static size_t set_bytes[4] = {0, 0, 0, 0};
-        std::lock_guard<std::mutex> lock(mu);
-        size_t& cur = set_bytes[(args.prof ? 2 : 0) + (shard ? 1 : 0)];
-        if (smem > cur) {
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            cur = smem;
-        }
+        cudaError_t e = raise_smem(smem, args.prof != nullptr, shard);
+        if (e != cudaSuccess) return e;
     }
     QbArgs copy = args;
     void* kargs[] = {&copy};

@@ -152,6 +152,7 @@ struct QbArgs {
     int* status;
     unsigned long long* prof;
     long long* hang;       // [8] mapped host memory: watchdog report (what+1, CTA, block, 4 values)
+    const volatile int* yield;  // mapped host flag: stop at the next sweep end (resumable); NULL = never
     int nbuf;              // cell buffers: 2 = next block's cells built during the colours
     int ring_stages;       // cp.async row-ring depth (2, 4 or 6)
     int colour_warps_min;  // lower bound on the colour group's warps (tuning)
@@ -165,20 +166,26 @@ size_t qblock_smem_bytes(int chain_warps, int p, int nblk, int share, int D, int
                          int ring_stages);
 int qblock_colour_warps(int chain_warps, int share, int D);
 cudaError_t launch_pcd_qblock(const QbArgs& args, int nblk, cudaStream_t st);
+// Raise the variant's dynamic shared-memory limit to smem now (solver creation), so no launch
+// has to set the attribute while another fit runs.
+cudaError_t qblock_reserve_smem(int chain_warps, size_t smem);
 namespace qb4 {
 size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
 int colour_warps_host(int share, int D);
 cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st);
+cudaError_t reserve_smem(size_t smem);
 }
 namespace qb6 {
 size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
 int colour_warps_host(int share, int D);
 cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st);
+cudaError_t reserve_smem(size_t smem);
 }
 namespace qb8 {
 size_t smem_bytes(int p, int nblk, int share, int D, int tdiag_smem, int nbuf, int ring_stages);
 int colour_warps_host(int share, int D);
 cudaError_t launch(const QbArgs& args, int nblk, cudaStream_t st);
+cudaError_t reserve_smem(size_t smem);
 }
 
 // Lag cap for a slab width (bounded by the stage ring's shared memory) and m.

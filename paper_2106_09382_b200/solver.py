@@ -172,6 +172,7 @@ class Solver:
             _lib.check(L.concord_solver_create_sharded(int(p), int(device), int(n_blocks), int(n_shards),
                                                        ctypes.byref(h)))
         self._h = h
+        self._nblk = int(n_blocks)
         self.p = int(p)
         self.device = int(device)
         self.n = None
@@ -276,10 +277,46 @@ class Solver:
         secs = np.zeros(max_iter)
         rc = L.concord_solver_fit(self._h, ctypes.byref(prm), ctypes.byref(res), _lib.ptr(deltas),
                                   _lib.ptr(objs), _lib.ptr(secs))
-        _lib.check(rc, allow=(_lib.CONCORD_NOT_CONVERGED,))
+        _lib.check(rc, allow=(_lib.CONCORD_NOT_CONVERGED, _lib.CONCORD_YIELDED))
         self.last_result = res
         k = res.iterations
         return rc, res, deltas[:k], objs[:k], secs[:k]
+
+    def request_yield(self, on=True):
+        """Ask the blocked fit running on this solver (or its next one) to stop at the end of its
+        current sweep unless that sweep converged or hit the cap: fit_raw then returns
+        CONCORD_YIELDED and `take_state` on another solver continues it.  Thread-safe; stays set
+        until request_yield(False)."""
+        _lib.check(_lib.load().concord_solver_request_yield(self._h, 1 if on else 0))
+
+    def take_state(self, src):
+        """Continue src's yielded fit here: Omega and W = Omega T move slab layout to slab layout on
+        the device; the next fit_raw resumes from them (bitwise the uninterrupted fit)."""
+        _lib.check(_lib.load().concord_solver_take_state(self._h, src._h))
+
+    def reserve(self, max_iter):
+        """Allocate the scratch and the records of fits up to max_iter sweeps now (a solver that
+        joins a running path must not allocate on the way: that can wait for the other kernels)."""
+        _lib.check(_lib.load().concord_solver_reserve(self._h, int(max_iter)))
+
+    def copy_gram(self, src):
+        """T and n from another solver of the same p on the same device (device to device)."""
+        _lib.check(_lib.load().concord_solver_copy_gram(self._h, src._h))
+        self.n = src.n
+
+    def export_state(self):
+        """(Omega, W) of the last fit as host arrays (p x p each)."""
+        om, w = np.empty((self.p, self.p)), np.empty((self.p, self.p))
+        _lib.check(_lib.load().concord_solver_export_state(self._h, _lib.ptr(om), _lib.ptr(w), _lib.HOST))
+        return om, w
+
+    def import_state(self, om, w):
+        """The next fit continues from (Omega, W) (host p x p arrays, e.g. from export_state)."""
+        om = np.ascontiguousarray(om, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        if om.shape != (self.p, self.p) or w.shape != (self.p, self.p):
+            raise DimensionError(f"state must be {self.p} x {self.p}")
+        _lib.check(_lib.load().concord_solver_import_state(self._h, _lib.ptr(om), _lib.ptr(w), _lib.HOST))
 
     def omega(self, out=None):
         if out is None:
@@ -320,7 +357,15 @@ class Solver:
         return ii, jj, vv
 
     def fit(self, lam, delta_tol=1e-5, max_iter=200, init=None, trace=True, raise_on_cap=True) -> FitReport:
-        rc, res, deltas, objs, secs = self.fit_raw(lam, delta_tol, max_iter, init, trace)
+        return self.report([self.fit_raw(lam, delta_tol, max_iter, init, trace)], trace, raise_on_cap)
+
+    def report(self, segments, trace=True, raise_on_cap=True) -> FitReport:
+        """FitReport of the fit whose last segment ran here: `segments` are fit_raw results, one per
+        solver the fit ran on (PathScheduler hand-over), traces concatenated in order."""
+        rc, res = segments[-1][0], segments[-1][1]
+        deltas = np.concatenate([sg[2] for sg in segments])
+        objs = np.concatenate([sg[3] for sg in segments])
+        secs = np.concatenate([sg[4] for sg in segments])
         om = self.omega()
         # A converged fit's estimate is exactly symmetric with a positive diagonal by construction
         # (both mirrored cells get the same value; the diagonal closed form is positive).  A fit
@@ -328,7 +373,7 @@ class Solver:
         # reference's _finish does (solver.py:214-224 -> model.py:117-120), which raises.
         report = FitReport(
             estimate=PrecisionEstimate._trusted(om) if res.converged else PrecisionEstimate(om),
-            iterations=int(res.iterations),
+            iterations=int(sum(int(sg[1].iterations) for sg in segments)),
             final_delta=float(res.final_delta),
             converged=bool(res.converged),
             objective_trace=tuple(float(v) for v in objs) if trace else (),
@@ -350,8 +395,9 @@ def pcd_path(x_or_gram, lams, delta_tol=1e-5, max_outer_iterations=200, warm_sta
     (a non-converged fit is returned with converged=False, not raised).
 
     concurrency=k (cold mode) runs the fits on k lanes, each a solver on its
-    own share of the SMs (k=3 on a B200: 66/41/41; k=4: 66/28/27/27, the bench's), densest lambda first
-    (`PathScheduler`); the results are bitwise those of sequential fits.
+    own share of the SMs (k=3 on a B200: 66/41/41; k=4: 66/28/27/27, the bench's), densest lambda first,
+    lanes that run dry handing their SMs to the fits still running (`PathScheduler.run_segmented`);
+    the results are bitwise those of sequential fits.
     """
     if concurrency > 1:
         if warm_start:
@@ -433,6 +479,11 @@ class PathScheduler:
         self.p, self.device, self.k, self.lanes = int(p), int(device), len(lanes), lanes
         self._full = None  # all-SM solver, created when a path has a single fit (or k <= 1)
         self._gram = None
+        self._spare = {}  # CTA count -> idle solvers that continue a fit on a lane grown by hand-over
+        self._spare_lock = threading.Lock()
+        self._gram_gen = 0
+        self._spare_made = False
+        self.handovers = 0  # fits moved to a larger solver (last run_segmented call)
 
     @property
     def full(self):
@@ -444,16 +495,49 @@ class PathScheduler:
 
     @property
     def solvers(self):
-        return self.shares + ([self._full] if self._full is not None else [])
+        spare = [s for v in self._spare.values() for s in v]
+        return self.shares + ([self._full] if self._full is not None else []) + spare
 
     def close(self):
         for s in self.solvers:
             s.close()
 
+    SPARE_BYTES = 16 << 30  # device memory the hand-over solvers may take
+    RESERVE_SWEEPS = 5000  # per-sweep records the hand-over solvers allocate up front
+
     def set_gram(self, gram):
         self._gram = gram
-        for s in self.solvers:
+        self._gram_gen += 1  # the hand-over solvers copy T from a lane when next used
+        for s in self.shares + ([self._full] if self._full is not None else []):
             s.set_gram(gram)
+        if self.k > 1 and not self._spare_made:
+            self._make_spares()
+
+    def _make_spares(self):
+        """One solver for every SM count a lane can grow to by hand-over (sums of two or more
+        lanes), largest first, within SPARE_BYTES: created once, so a hand-over costs a state move
+        (~1 ms at p=5000), not an allocation."""
+        import itertools
+
+        self._spare_made = True
+        sums = set()
+        for r in range(2, self.k + 1):
+            for c in itertools.combinations(self.lanes, r):
+                sums.add(sum(c))
+        per = 3 * 8 * self.p * self.p * 1.1
+        budget = self.SPARE_BYTES
+        try:
+            for v in sorted(sums, reverse=True):
+                if per > budget:
+                    break
+                sv = Solver(self.p, device=self.device, n_blocks=v)
+                sv._gen = -1
+                sv.reserve(self.RESERVE_SWEEPS)
+                self._spare.setdefault(v, []).append(sv)
+                budget -= per
+        except _lib.ConcordError as e:
+            if getattr(e, "code", None) != _lib.CONCORD_ERR_OOM:
+                raise
 
     def run(self, lams, fit_one):
         """fit_one(solver, lam) -> result; returns the results in the order of `lams`."""
@@ -489,6 +573,128 @@ class PathScheduler:
             raise errors[0]
         return out
 
+    def _take_spare(self, nblk):
+        with self._spare_lock:
+            idle = self._spare.get(nblk)
+            return idle.pop() if idle else None
+
+    def _return_spare(self, s):
+        with self._spare_lock:
+            self._spare.setdefault(s._nblk, []).append(s)
+
+    def run_segmented(self, lams, fit_seg, finish, handover=True):
+        """The lanes of `run`, plus hand-over: when the queue is empty, a lane that finishes gives
+        its SMs to the lane running the densest remaining fit, which stops at its next sweep end
+        (Solver.request_yield) and continues on an idle solver of its grown SM count (take_state;
+        `_make_spares` holds one per reachable count).  The last fits of a path therefore end on
+        most of the device instead of on their lanes.
+
+        fit_seg(solver, lam, done) -> (rc, iterations, payload): one segment of a fit (done = sweeps
+        run by its earlier segments); finish(solver, lam, payloads) -> result, called on the solver
+        that ran the last segment before anything else uses it.  Results are bitwise those of
+        uninterrupted fits (W is carried, and the slab count never changes the bits)."""
+        import threading
+
+        lams = list(lams)
+        out = [None] * len(lams)
+        self.handovers = 0
+        if self.k <= 1 or len(lams) <= 1:
+            for i, lam in enumerate(lams):
+                rc, _, pl = fit_seg(self.full, lam, 0)
+                out[i] = finish(self.full, lam, [pl])
+            return out
+        handover = bool(handover) and self._gram_gen > 0
+        queue = sorted(range(len(lams)), key=lambda i: lams[i])  # densest first
+        lock = threading.Lock()
+        errors = []
+        first = {j: queue.pop(0) for j in range(min(self.k, len(queue)))}
+        grant = {j: self.lanes[j] for j in range(self.k)}  # SMs each lane may use
+        free = [0]  # SMs of finished lanes that no running fit could take yet
+        running = {}  # lane -> (lambda index, solver it runs on; None while moving)
+        claim = {}  # lane -> the idle solver of its grown SM count it moves to at its next yield
+        lib = _lib.load()
+
+        def donate(j):  # under lock: lane j ran dry
+            free[0] += grant[j]
+            grant[j] = 0
+            for r in sorted(running, key=lambda r: lams[running[r][0]]):  # densest first
+                nxt = self._take_spare(grant[r] + free[0])
+                if nxt is None:
+                    continue
+                if r in claim:
+                    self._return_spare(claim.pop(r))
+                claim[r] = nxt
+                grant[r] += free[0]
+                free[0] = 0
+                if running[r][1] is not None:
+                    running[r][1].request_yield(True)
+                return
+
+        def lane(j):
+            cur = self.shares[j]
+            stream = lib.concord_solver_stream(cur._h)
+            try:
+                i = first.get(j)
+                while i is not None:
+                    pls, done = [], 0
+                    with lock:
+                        running[j] = (i, cur)
+                    while True:
+                        rc, it, pl = fit_seg(cur, lams[i], done)
+                        pls.append(pl)
+                        done += it
+                        with lock:
+                            cur.request_yield(False)
+                            nxt = claim.pop(j, None)
+                            if rc == _lib.CONCORD_YIELDED:
+                                running[j] = (i, None)  # moving: donors only re-claim
+                        if rc != _lib.CONCORD_YIELDED:
+                            if nxt is not None:  # the fit ended before it could move
+                                self._return_spare(nxt)
+                            break
+                        if nxt is None:  # (not expected) continue in place
+                            cur.take_state(cur)
+                            continue
+                        nxt.request_yield(False)
+                        nxt.set_stream(stream)
+                        if nxt._gen != self._gram_gen:
+                            nxt.copy_gram(cur)
+                            nxt._gen = self._gram_gen
+                        nxt.take_state(cur)
+                        if cur is not self.shares[j]:
+                            self._return_spare(cur)
+                        cur = nxt
+                        with lock:
+                            running[j] = (i, cur)
+                            self.handovers += 1
+                            if j in claim:  # grown again while moving
+                                cur.request_yield(True)
+                    out[i] = finish(cur, lams[i], pls)
+                    with lock:
+                        running.pop(j, None)
+                        i = queue.pop(0) if queue and not errors else None
+                        if i is None and handover:
+                            donate(j)
+            except BaseException as e:  # re-raised in the caller's thread
+                errors.append(e)
+            finally:
+                if cur is not self.shares[j]:
+                    self._return_spare(cur)
+                with lock:
+                    if j in claim:
+                        self._return_spare(claim.pop(j))
+
+        threads = [threading.Thread(target=lane, args=(j,)) for j in range(self.k)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for s in self.shares:
+            s.request_yield(False)
+        if errors:
+            raise errors[0]
+        return out
+
 
 def _path_concurrent(x_or_gram, lams, delta_tol, max_outer_iterations, device, trace, k):
     if isinstance(x_or_gram, DataMatrix):
@@ -500,8 +706,12 @@ def _path_concurrent(x_or_gram, lams, delta_tol, max_outer_iterations, device, t
     key = ("path", gram.p, int(device), int(k))
     with _checkout(key, lambda: PathScheduler(gram.p, device=device, k=k)) as sched:
         sched.set_gram(gram)
-        return sched.run(lams, lambda s, lam: s.fit(lam, delta_tol, max_outer_iterations, trace=trace,
-                                                    raise_on_cap=False))
+
+        def seg(s, lam, done):
+            r = s.fit_raw(lam, delta_tol, max_outer_iterations - done, trace=trace)
+            return r[0], int(r[1].iterations), r
+
+        return sched.run_segmented(lams, seg, lambda s, lam, segs: s.report(segs, trace, raise_on_cap=False))
 
 
 def _gram_p(x):
