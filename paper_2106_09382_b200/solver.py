@@ -508,8 +508,13 @@ class PathScheduler:
     def set_gram(self, gram):
         self._gram = gram
         self._gram_gen += 1  # the hand-over solvers copy T from a lane when next used
-        for s in self.shares + ([self._full] if self._full is not None else []):
-            s.set_gram(gram)
+        # one host upload; the other lanes copy T device to device (each its own slab layout)
+        own = self.shares + ([self._full] if self._full is not None else [])
+        for i, s in enumerate(own):
+            if i == 0:
+                s.set_gram(gram)
+            else:
+                s.copy_gram(own[0])
         if self.k > 1 and not self._spare_made:
             self._make_spares()
 
