@@ -122,16 +122,37 @@ def test_scheduler_hands_idle_lanes_to_the_dense_fit():
     sched = cb.PathScheduler(p, k=2, lanes=[74, 74])
     sched.set_gram(g)
 
+    import threading
+    import time
+
+    sparse_done = threading.Event()
+
     def seg(s, lam, done):
+        if lam == lams[0] and done == 0 and gate[0]:
+            # the dense fit starts only after the sparse lane ran dry and handed its SMs over (the
+            # donation follows the sparse lane's finish in the same thread): deterministic hand-over
+            sparse_done.wait(60)
+            time.sleep(0.2)
         r = s.fit_raw(lam, 1e-5, 500 - done)
         return r[0], int(r[1].iterations), (r, s.layout())
 
+    nfin = []
+
     def fin(s, lam, pls):
+        if lam != lams[0]:
+            nfin.append(lam)
+            if len(nfin) == 2:  # both sparse fits done (on the other lane): the queue is empty
+                sparse_done.set()
         return s.report([x[0] for x in pls], raise_on_cap=False), [x[1] for x in pls]
 
+    gate = [True]
     out = sched.run_segmented(lams, seg, fin)
     assert sched.handovers >= 1
-    assert any(len(lays) >= 2 for _, lays in out)  # a fit ran on at least two solvers
+    dense, lays = out[0]
+    # yielded after its first sweep and finished on the full-device solver (narrower slabs)
+    assert len(lays) >= 2 and lays[-1]["slab_width"] < lays[0]["slab_width"]
+    gate[0] = False
+    sparse_done.clear()
     for a, (b, _) in zip(seq, out):
         assert a.iterations == b.iterations
         assert np.array_equal(a.estimate.omega, b.estimate.omega)
