@@ -149,7 +149,8 @@ int concord_solver_export_state(concord_solver* s, double* omega_out, double* w_
 int concord_solver_import_state(concord_solver* s, const double* omega, const double* w, int32_t where);
 /* The two steps above device to device: dst (same p, device and Gram, any slab count) continues
  * src's yielded fit with its next concord_solver_fit.  Enqueued on dst's stream after src's
- * stream drained; src is unchanged.  dst == src: the next fit resumes in place. */
+ * stream drained, and complete on return (src is free for other work); src is unchanged.
+ * dst == src: the next fit resumes in place. */
 int concord_solver_take_state(concord_solver* dst, concord_solver* src);
 /* Allocate now what fits of up to max_iter sweeps and state moves allocate lazily (the p x p
  * scratch, the per-sweep records): a solver that joins a running path must not allocate (or

@@ -683,6 +683,8 @@ int concord_solver_take_state(concord_solver* dst, concord_solver* src) {
         CK(launch_pack_slabs(dst->stage, dst->p, to[k], dst->p, dst->w, dst->ss, dst->ld, dst->nblk_launch, dst->blk0,
                              dst->stream));
     }
+    // src is free for other work once this returns (the scheduler hands it to another lane)
+    CK(cudaStreamSynchronize(dst->stream));
     dst->resume = true;
     return CONCORD_OK;
 }
