@@ -167,3 +167,33 @@ def test_scheduler_hands_idle_lanes_to_the_dense_fit():
     out3 = sched.run_segmented(lams, seg, fin, handover=False)
     assert sched.handovers == 0 and all(len(l) == 1 for _, l in out3)
     sched.close()
+
+
+def test_state_through_device_pointers():
+    """concord_solver_export_state / import_state with CONCORD_DEVICE buffers (torch tensors)."""
+    import torch
+
+    p, lam = 800, 0.15
+    g = _problem(p, seed=9)
+    ref, _, _ = _uninterrupted(g, lam)
+    a, b = cb.Solver(p, n_blocks=30), cb.Solver(p, n_blocks=120)
+    a.set_gram(g)
+    b.set_gram(g)
+    a.request_yield(True)
+    s1 = a.fit_raw(lam, 1e-5, 300)
+    a.request_yield(False)
+    assert s1[0] == _lib.CONCORD_YIELDED
+    om = torch.empty((p, p), dtype=torch.float64, device="cuda")
+    w = torch.empty((p, p), dtype=torch.float64, device="cuda")
+    L = _lib.load()
+    _lib.check(L.concord_solver_export_state(a._h, om.data_ptr(), w.data_ptr(), _lib.DEVICE))
+    torch.cuda.synchronize()
+    om_h, w_h = a.export_state()
+    assert np.array_equal(om.cpu().numpy(), om_h) and np.array_equal(w.cpu().numpy(), w_h)
+    _lib.check(L.concord_solver_import_state(b._h, om.data_ptr(), w.data_ptr(), _lib.DEVICE))
+    s2 = b.fit_raw(lam, 1e-5, 300 - s1[1].iterations)
+    rep = b.report([s1, s2], raise_on_cap=False)
+    assert rep.iterations == ref.iterations
+    assert np.array_equal(rep.estimate.omega, ref.estimate.omega)
+    a.close()
+    b.close()
