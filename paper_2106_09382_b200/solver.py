@@ -461,6 +461,9 @@ class PathScheduler:
             try:
                 for v in lanes:
                     self.shares.append(Solver(p, device=device, n_blocks=v))
+                    # records allocated now: a lane's first fit must not allocate (or free) device
+                    # memory while the other lanes' kernels run -- that waits for them
+                    self.shares[-1].reserve(self.RESERVE_SWEEPS)
                 # kernel variant per lane (Solver.set_chain_warps).  Alone, an apply-heavy dense fit
                 # and chain-heavy sparse fits are 6% / 11% faster, but running concurrently every
                 # combination was slower than the default (profiles/r02/lanes_variants.log), so the
