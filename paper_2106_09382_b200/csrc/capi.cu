@@ -32,6 +32,7 @@ int fail(int code, const char* fmt, ...) {
     do {                                                                                           \
         cudaError_t _e = (expr);                                                                   \
         if (_e != cudaSuccess) {                                                                   \
+            (void)cudaGetLastError(); /* reported here, not again by the next launch check */      \
             return fail(_e == cudaErrorMemoryAllocation ? CONCORD_ERR_OOM : CONCORD_ERR_CUDA,      \
                         "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e));        \
         }                                                                                          \
@@ -52,7 +53,11 @@ template <typename T>
 cudaError_t dalloc(T** ptr, size_t count) {
     *ptr = nullptr;
     if (count == 0) count = 1;
-    return cudaMalloc((void**)ptr, sizeof(T) * count);
+    const cudaError_t e = cudaMalloc((void**)ptr, sizeof(T) * count);
+    // a failed allocation also sets the runtime's last error, which the next kernel launch's
+    // cudaGetLastError() would report as its own failure: the caller gets the error here instead
+    if (e != cudaSuccess) (void)cudaGetLastError();
+    return e;
 }
 
 int check_device(int32_t device) {
@@ -446,7 +451,7 @@ int create_common(int64_t p, int32_t device, int32_t n_blocks, int32_t n_shards,
 #define CKC(expr)                                                                                  \
     do {                                                                                           \
         cudaError_t _e = (expr);                                                                   \
-        if (_e != cudaSuccess)                                                                     \
+        if (_e != cudaSuccess && ((void)cudaGetLastError(), true))                                 \
             return cleanup(fail(_e == cudaErrorMemoryAllocation ? CONCORD_ERR_OOM : CONCORD_ERR_CUDA, \
                                 "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e))); \
     } while (0)

@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 
 import paper_2106_09382_b200 as cb
-from paper_2106_09382_b200 import synth
+from paper_2106_09382_b200 import _lib, synth
 
 pytestmark = pytest.mark.gpu
 
@@ -110,3 +110,16 @@ def test_path_lanes_with_competing_kernels_on_the_device():
     for r, w in zip(reps, want):
         assert r.iterations == w.iterations
         assert np.array_equal(r.estimate.omega, w.estimate.omega)
+
+
+def test_failed_allocation_does_not_poison_the_next_launch():
+    """A device allocation that fails (OOM) is reported by the call that made it; the runtime's
+    last-error slot is cleared, so the next kernel launch's error check does not report it again."""
+    with pytest.raises(_lib.ConcordError) as ei:
+        cb.Solver(200_000)  # 3 x 320 GB of slabs
+    assert ei.value.code == _lib.CONCORD_ERR_OOM
+    x = synth.sample_scale_free_device(40, 1000, seed=1, truth_seed=0)  # allocates and launches
+    assert x.shape == (1000, 40)
+    _, t = synth.problem("ar2", 200, 400, seed=2)
+    rep = cb.pcd_fit(cb.GramMatrix(t, 400), cb.SolverConfig(lam=0.3))
+    assert rep.converged
