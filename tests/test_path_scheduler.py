@@ -70,6 +70,9 @@ def test_default_lane_splits(monkeypatch):
         def set_chain_warps(self, cw):
             pass
 
+        def reserve(self, max_iter):
+            pass
+
     monkeypatch.setattr(solver._lib, "device_sm_count", lambda device: 148)
     monkeypatch.setattr(solver, "Solver", FakeSolver)
     assert PathScheduler(5000, k=2).lanes == [74, 74]
