@@ -130,7 +130,8 @@ int concord_solver_gram_from_raw_data(concord_solver* s, const double* X, int64_
 int concord_solver_get_gram(concord_solver* s, double* T_out, int32_t where);
 /* pcd_fit (solver.py:254-294).  delta_trace / objective_trace / sweep_seconds
  * may be NULL, else hold max_iter doubles.  Returns CONCORD_NOT_CONVERGED when
- * the cap is hit (results valid, like NotConverged.report). */
+ * the cap is hit (results valid, like NotConverged.report), and CONCORD_YIELDED
+ * when concord_solver_request_yield stopped it at a sweep end (below). */
 int concord_solver_fit(concord_solver* s, const concord_fit_params* prm, concord_fit_result* res,
                        double* delta_trace, double* objective_trace, double* sweep_seconds);
 int concord_solver_get_omega(concord_solver* s, double* omega_out, int32_t where);
