@@ -1,3 +1,8 @@
+#!/bin/bash
+# A/B of two builds of the library in one gpurun call: copy the baseline build to
+# paper_2106_09382_b200/libconcord_base.so (git-ignored, travels with the snapshot), rebuild the
+# candidate in place, run this.  Single fits on a 27-SM lane and the full device, the dense fit on
+# a 66-SM lane, and the bench path on 4 lanes (profiles/r02/ab_speculative_T_loads.log).
 for lib in base new; do
   if [ $lib = base ]; then export CONCORD_LIB_PATH=$PWD/paper_2106_09382_b200/libconcord_base.so; else unset CONCORD_LIB_PATH; fi
   echo "== $lib"
